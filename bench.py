@@ -1,0 +1,496 @@
+"""bench.py -- GPU-actor path of arXiv 1611.03226 (dynflow) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload motion720|motion4k|dpd1|dpd3|dpd5]
+
+Default workload = BASELINE.json configs[1]: motion detection on 1280x720
+RGB, 300 synthetic frames per GPU (frame-range sharded; one-frame halo from
+the previous rank over NCCL P2P, no collective on the data path).  One
+step = one firing of the fused motion actor over the rank's 300 frames.
+
+--impl reference times the reference's own CPU implementation (the dynflow
+network compiled from /root/reference into oracle/_ref, or the oracle port
+when that is absent) on the box's host cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HBM_FALLBACK_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+FP32_PEAK_TOPS = 148 * 128 * 1.965e9 / 1e12  # non-fused FP32 issue peak at max clock
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+
+
+WORKLOADS = {
+    # name: (kind, params)
+    "motion720": ("motion", dict(w=1280, h=720, frames=300, fmt=3, thr=32,
+                                 label="Motion detection 1280x720 RGB, 300 synthetic frames per GPU")),
+    "motion4k": ("motion", dict(w=3840, h=2160, frames=40, fmt=3, thr=32,
+                                label="Motion detection 3840x2160 RGB, 40 frames per GPU (320 at 8 GPUs)")),
+    "dpd1": ("dpd", dict(samples=1 << 20, period=65536, T=10, sched="first2",
+                         label="DPD 2 branches x 10-tap, 2^20 samples, fixed config")),
+    "dpd3": ("dpd", dict(samples=1 << 26, period=4096, T=10, sched="ramp",
+                         label="DPD dynamic 1->10 branches per 4096-sample block (ramp), 2^26 samples")),
+    "dpd5": ("dpd", dict(samples=1 << 27, period=65536, T=32, sched="all10",
+                         label="DPD 10 branches x 32-tap, 2^27 samples per GPU (2^30 at 8 GPUs)")),
+}
+
+
+# ------------------------------------------------------------------ helpers
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            parts = [p.strip() for p in l.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        loaded = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def traffic_from_profiles(kernel: str, workload: str):
+    """dram bytes per launch from the committed ncu summary, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as fh:
+        d = json.load(fh)
+    return d.get(workload, {}).get(kernel)
+
+
+# ------------------------------------------------------------------ ours
+def bench_motion_ours(args, p, rank, world, local):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1611_03226_b200 import _lib, device, motion
+
+    _lib.require_gpu()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    W, H, F, fmt = p["w"], p["h"], p["frames"], p["fmt"]
+    in_frame, out_frame = W * H * fmt, W * H
+    stream = torch.cuda.current_stream()
+    sh = C.c_void_p(stream.cuda_stream)
+    inp = torch.empty(F * in_frame, dtype=torch.uint8, device=dev)
+    out = torch.empty(F * out_frame, dtype=torch.uint8, device=dev)
+    halo = torch.empty(in_frame, dtype=torch.uint8, device=dev)
+    _lib.call("df_fill_random_u8", C.c_void_p(inp.data_ptr()), inp.numel(), 1234 + rank, sh)
+    actor = motion.MotionActor(W, H, fmt, p["thr"], device=local)
+
+    def step(ev_k0=None, ev_k1=None):
+        if world > 1:
+            # One-frame halo: the previous rank's last input frame (NCCL P2P).
+            ops = []
+            if rank + 1 < world:
+                ops.append(dist.P2POp(dist.isend, inp[(F - 1) * in_frame:], rank + 1))
+            if rank > 0:
+                ops.append(dist.P2POp(dist.irecv, halo, rank - 1))
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+        if rank > 0:
+            _lib.call("df_motion_set_prev_frame", actor.handle, C.c_void_p(halo.data_ptr()), sh)
+        else:
+            _lib.call("df_motion_set_prev_frame", actor.handle, None, sh)
+        if ev_k0 is not None:
+            ev_k0.record(stream)
+        _lib.call("df_motion_fire", actor.handle, C.c_void_p(inp.data_ptr()), C.c_void_p(out.data_ptr()), F, sh)
+        if ev_k1 is not None:
+            ev_k1.record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = device.kernel_launches()
+    with ClockSampler(local) as clk:
+        t0.record(stream)
+        for i in range(args.steps):
+            step(*kev[i])
+        t1.record(stream)
+        torch.cuda.synchronize()
+    launches = device.kernel_launches() - launches0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / args.steps
+    kms = statistics.mean(a.elapsed_time(b) for a, b in kev)
+    ms, kms = max_over_ranks(ms, world), max_over_ranks(kms, world)
+
+    # e2e through the C-ABI host-buffer call: pinned H2D + fire + D2H per step.
+    hin = device.PinnedArray(F * in_frame, np.uint8)
+    hout = device.PinnedArray(F * out_frame, np.uint8)
+    hin.array[:] = np.frombuffer(np.random.default_rng(rank).bytes(F * in_frame), np.uint8)
+    actor.run_host(hin.array, hout.array)  # warm
+    e2e_t = []
+    for _ in range(max(2, min(args.steps, 5))):
+        torch.cuda.synchronize()
+        a = time.perf_counter()
+        actor.run_host(hin.array, hout.array)
+        e2e_t.append(time.perf_counter() - a)
+    e2e_s = max_over_ranks(statistics.median(e2e_t), world)
+    torch.cuda.synchronize()
+
+    value = world * F / (ms / 1e3)
+    bytes_alg = 4.0 * W * H * F if fmt == 3 else 2.0 * W * H * F
+    achieved = bytes_alg / (kms / 1e3) / 1e9
+    hbm, hbm_src = peaks()
+    traffic = traffic_from_profiles("motion_fused_kernel", args.workload)
+    res = {
+        "metric": "motion-detect frames/s",
+        "value": round(value, 1),
+        "unit": "frames/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u8",
+        "data": "synthetic (device splitmix64 bytes; RGB interleaved)",
+        "config": {"workload": p["label"], "width": W, "height": H, "frames_per_gpu": F,
+                   "threshold": p["thr"], "input": "rgb" if fmt == 3 else "gray",
+                   "chain": "gray->gauss5x5->|cur-prev|>thr->median5 (reference-pinned)",
+                   "parallelism": f"frame-range shards x{world}, 1-frame halo via NCCL P2P",
+                   "l2": f"inputs {F * in_frame / 1e6:.0f} MB per GPU > 126 MB L2 (no flush needed)"},
+        "e2e": {"value": round(world * F / e2e_s, 1), "unit": "frames/s",
+                "h2d_bytes_per_step": F * in_frame, "d2h_bytes_per_step": F * out_frame,
+                "path": "df_motion_run_host (C ABI, pinned host buffers, chunked H2D/fire/D2H)"},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                     "frac": round(achieved / hbm, 4), "traffic": traffic,
+                     "kernel": "motion_fused_kernel", "kernel_ms": round(kms, 4),
+                     "algorithmic_bytes_per_launch": bytes_alg, "peak_source": hbm_src},
+        "clocks": clk.summary(),
+    }
+    return res
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def dpd_schedule(kind: str, blocks: int) -> np.ndarray:
+    if kind == "first2":
+        return np.array([0b11], np.uint16)
+    if kind == "all10":
+        return np.array([0x3FF], np.uint16)
+    if kind == "ramp":
+        return np.array([(1 << (1 + i % 10)) - 1 for i in range(10)], np.uint16)
+    raise ValueError(kind)
+
+
+def dpd_flops_per_sample(sched: np.ndarray, T: int) -> float:
+    # B*(8T+4) + B_max + 3 per sample (+1 sqrt), mean over the schedule
+    tot = 0.0
+    for m in sched:
+        B = bin(int(m)).count("1")
+        bmax = int(m).bit_length()
+        tot += B * (8 * T + 4) + bmax + 3
+    return tot / len(sched)
+
+
+def bench_dpd_ours(args, p, rank, world, local):
+    import torch
+    import torch.distributed as dist
+
+    from oracle import oracle as _unused  # noqa: F401  (not used: inputs are device-synthetic)
+    from paper_1611_03226_b200 import _lib, device, dpd
+
+    _lib.require_gpu()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    N, period, T = p["samples"], p["period"], p["T"]
+    blocks = N // period
+    sched = dpd_schedule(p["sched"], blocks)
+    stream = torch.cuda.current_stream()
+    sh = C.c_void_p(stream.cuda_stream)
+    x = torch.empty(2 * N, dtype=torch.float32, device=dev)
+    y = torch.empty(2 * N, dtype=torch.float32, device=dev)
+    ctrl = torch.empty(blocks, dtype=torch.int32, device=dev)
+    _lib.call("df_fill_random_pm1", C.c_void_p(x.data_ptr()), 2 * N, 99 + rank, sh)
+    taps = np.random.default_rng(808).uniform(-0.5, 0.5, size=(10, T, 2)).astype(np.float32)
+    actor = dpd.DpdActor(period, taps, device=local)
+    sched_np = np.ascontiguousarray(sched)
+    _lib.call("df_dpd_config_tokens", local, sched_np.ctypes.data_as(C.c_void_p), sched_np.size, 0, blocks,
+              C.c_void_p(ctrl.data_ptr()), sh)
+
+    def step(ev0=None, ev1=None):
+        if ev0 is not None:
+            ev0.record(stream)
+        _lib.call("df_dpd_fire", actor.handle, C.c_void_p(ctrl.data_ptr()), C.c_void_p(x.data_ptr()),
+                  C.c_void_p(y.data_ptr()), blocks, sh)
+        if ev1 is not None:
+            ev1.record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = device.kernel_launches()
+    with ClockSampler(local) as clk:
+        t0.record(stream)
+        for i in range(args.steps):
+            step(*kev[i])
+        t1.record(stream)
+        torch.cuda.synchronize()
+    launches = device.kernel_launches() - launches0
+    ms = max_over_ranks(t0.elapsed_time(t1) / args.steps, world)
+    kms = max_over_ranks(statistics.mean(a.elapsed_time(b) for a, b in kev), world)
+    actor.check()
+
+    hin = device.PinnedArray(2 * N, np.float32)
+    hout = device.PinnedArray(2 * N, np.float32)
+    hin.array[:] = np.random.default_rng(rank).uniform(-1, 1, 2 * N).astype(np.float32)
+    actor.run_host(hin.array, hout.array, sched)
+    e2e_t = []
+    for _ in range(max(2, min(args.steps, 5))):
+        a = time.perf_counter()
+        actor.run_host(hin.array, hout.array, sched)
+        e2e_t.append(time.perf_counter() - a)
+    e2e_s = max_over_ranks(statistics.median(e2e_t), world)
+
+    fps = dpd_flops_per_sample(sched, T)
+    achieved_tops = N * fps / (kms / 1e3) / 1e12
+    hbm, _ = peaks()
+    return {
+        "metric": "DPD Msamples/s",
+        "value": round(world * N / (ms / 1e3) / 1e6, 1),
+        "unit": "Msamples/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (device uniform[-1,1) complex samples)",
+        "config": {"workload": p["label"], "samples_per_gpu": N, "period": period, "taps_per_branch": T,
+                   "schedule": p["sched"], "parallelism": f"block-range shards x{world}",
+                   "l2": f"in+out {16 * N / 1e6:.0f} MB per GPU"},
+        "e2e": {"value": round(world * N / e2e_s / 1e6, 1), "unit": "Msamples/s",
+                "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * N,
+                "path": "df_dpd_run_host (C ABI, pinned host buffers)"},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "fp32", "achieved": round(achieved_tops, 2), "peak": round(FP32_PEAK_TOPS, 1),
+                     "unit": "Top/s (non-fused FP32)", "frac": round(achieved_tops / FP32_PEAK_TOPS, 4),
+                     "traffic": traffic_from_profiles("dpd_main_kernel", args.workload),
+                     "kernel_ms": round(kms, 4), "flops_per_sample": fps,
+                     "hbm_frac": round(16 * N / (kms / 1e3) / 1e9 / hbm, 4)},
+        "clocks": clk.summary(),
+    }
+
+
+# ------------------------------------------------------------------ CPU
+def cpu_motion(p, steps, warmup, threads=None, frames_per_net=None):
+    """Reference dynflow motion network (5 actor threads each) on gray(RGB),
+    several independent networks on disjoint frame ranges to use the host
+    cores; falls back to the single-thread oracle port."""
+    from oracle import oracle as O
+    W, H = p["w"], p["h"]
+    ncpu = os.cpu_count() or 1
+    if O.ref_available():
+        R = O.ref()
+        nets = threads or max(1, ncpu // 5)
+        fpn = frames_per_net or 8
+        rgb = O.synth_bytes(fpn * W * H * 3, 5)
+        outs = [np.empty(fpn * W * H, np.uint8) for _ in range(nets)]
+
+        def one(i):
+            gray = O.rgb_to_gray(rgb)
+            a, w_ = C.c_double(), C.c_double()
+            R.ref_motion_network(gray.ctypes.data_as(C.c_void_p), fpn, W, H, 32, 1,
+                                 outs[i].ctypes.data_as(C.c_void_p), C.byref(a), C.byref(w_))
+
+        times = []
+        for s in range(warmup + steps):
+            ts = [threading.Thread(target=one, args=(i,)) for i in range(nets)]
+            a = time.perf_counter()
+            for t in ts:
+                t.start()
+            for t in ts:
+                t.join()
+            if s >= warmup:
+                times.append(time.perf_counter() - a)
+        t = statistics.median(times)
+        return {"value": round(nets * fpn / t, 2), "unit": "frames/s", "cores": min(ncpu, 5 * nets),
+                "kind": "reference",
+                "sample": f"{nets} concurrent dynflow motion networks (5 actor threads each) x {fpn} frames "
+                          f"{W}x{H}, gray(RGB) conversion included; median of {steps}"}
+    rgb = O.synth_bytes(4 * W * H * 3, 5)
+    a = time.perf_counter()
+    O.motion_rgb(rgb, W, H)
+    t = time.perf_counter() - a
+    return {"value": round(4 / t, 2), "unit": "frames/s", "cores": 1, "kind": "port",
+            "sample": f"oracle port, 4 frames {W}x{H} RGB, 1 thread"}
+
+
+def cpu_dpd(p, steps, warmup):
+    from oracle import oracle as O
+    period, T = p["period"], p["T"]
+    n = min(p["samples"], max(period, 1 << 20))
+    n -= n % period
+    sched = dpd_schedule(p["sched"], n // period)
+    x = O.synth_samples(n, 810)
+    taps = O.random_taps(808, T)
+    ncpu = os.cpu_count() or 1
+    use_ref = O.ref_available() and T == 10 and all(bin(int(m)).count("1") >= 2 for m in sched)
+    times = []
+    for s in range(warmup + steps):
+        if use_ref:
+            R = O.ref()
+            out = np.empty_like(x)
+            a_, w_ = C.c_double(), C.c_double()
+            sc = np.ascontiguousarray(sched)
+            a = time.perf_counter()
+            rc = R.ref_dpd_network(x.ctypes.data_as(C.c_void_p), n, taps.ctypes.data_as(C.c_void_p),
+                                   sc.ctypes.data_as(C.c_void_p), sc.size, period, out.ctypes.data_as(C.c_void_p),
+                                   C.byref(a_), C.byref(w_))
+            el = time.perf_counter() - a
+            assert rc == 0
+        else:
+            a = time.perf_counter()
+            O.dpd(x, taps, sched, period)
+            el = time.perf_counter() - a
+        if s >= warmup:
+            times.append(el)
+    t = statistics.median(times)
+    if use_ref:
+        return {"value": round(n / t / 1e6, 2), "unit": "Msamples/s", "cores": min(ncpu, 15), "kind": "reference",
+                "sample": f"dynflow DPD network (15 actor threads), {n} samples, period {period}; median of {steps}"}
+    return {"value": round(n / t / 1e6, 2), "unit": "Msamples/s", "cores": 1, "kind": "port",
+            "sample": f"oracle port (1 thread; reference cannot run T={T} or k=1 masks), {n} samples"}
+
+
+def bench_reference(args, kind, p, rank, world):
+    if rank != 0:
+        return None
+    if kind == "motion":
+        cb = cpu_motion(p, args.steps, args.warmup)
+        metric, unit = "motion-detect frames/s", "frames/s"
+    else:
+        cb = cpu_dpd(p, args.steps, args.warmup)
+        metric, unit = "DPD Msamples/s", "Msamples/s"
+    return {"impl": "reference", "metric": metric, "value": cb["value"], "unit": unit, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8" if kind == "motion" else "f32", "data": "synthetic",
+            "config": {"workload": p["label"]}, "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="motion720", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank, world, local = dist_env()
+    kind, p = WORKLOADS[args.workload]
+
+    if args.impl == "reference":
+        res = bench_reference(args, kind, p, rank, world)
+        if res is not None:
+            print(json.dumps(res), flush=True)
+        return
+
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    res = (bench_motion_ours if kind == "motion" else bench_dpd_ours)(args, p, rank, world, local)
+    if rank == 0:
+        if world == 1 and not args.no_cpu_baseline:
+            res["cpu_baseline"] = (cpu_motion(p, 3, 1) if kind == "motion" else cpu_dpd(p, 3, 1))
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,728 @@
+// dpd.cu -- the dynamic parallel-Hammerstein predistortion actor on sm_100a.
+//
+// Replaces the reference's dynamic DPD network part: split actor
+// (proj/src/dpd.cpp:225-256), ten branch actors poly_branch -> fir10
+// (:60-121, :258-289) and the adder (:129-145, :293-331), which the
+// reference runs as 12 threads exchanging per-period tokens.  Here one GPU
+// actor firing covers a batch of blocks (one block = one period = one
+// token of the reference's dynamic part), each gated by one control token
+// consumed on the device.  Data never round-trips through split/adder
+// channels: the fan-out and the branch sum live in registers.
+//
+// Bit-exactness.  Every float op is the reference's, in its order, with no
+// FMA contraction (__fmul_rn/__fadd_rn/__fsub_rn, IEEE __fsqrt_rn):
+//   mag   = sqrt(re*re + im*im); scale_b = ((1*mag)*mag)... (b-1 muls)
+//           (dpd.cpp:69-71; scale_b = scale_{b-1}*mag is the same sequence)
+//   fir   acc += (tr*xr - ti*xi); acc += (tr*xi + ti*xr), k ascending
+//           from 0.0f (dpd.cpp:87-104)
+//   adder out = 0.0f; out += y_b for active b ascending (dpd.cpp:306-320)
+// Two provable shortcuts: the leading "0.0f +" of the FIR accumulator and
+// of the adder are dropped and a single "+ 0.0f" is applied to the final
+// sum.  x + (+0) == x for every x != -0, the reference sums can never be
+// -0 (they start at +0 and an exact-zero sum rounds to +0), and dropping a
+// leading +0 only changes the sign of intermediate zeros -- so the final
+// "+ 0.0f" restores bit-identical output.
+//
+// FIR history across blocks.  Branch b's history at block p is the last
+// T-1 poly outputs of b's *active* stream before p (frozen while gated
+// off, dpd.cpp:264-279, fir10's chaining for short blocks :108-120).  A
+// prep kernel scans the batch's control tokens on the device (per branch:
+// compacted list of active blocks), resolves each needed history sample to
+// either an earlier block's input (poly recomputed -- it is memoryless) or
+// the carried FirState, and writes a small per-(block, branch) history
+// table.  All blocks of the batch then run fully in parallel.
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "channel_dev.cuh"
+#include "channel_host.hpp"
+#include "common.cuh"
+
+namespace df {
+namespace {
+
+constexpr int kBranches = 10;
+constexpr int kMaxTaps = 32;
+
+struct DpdIO {
+  // Raw mode: direct pointers.  Channel mode: resolved from the device
+  // phases at kernel start (chan_*_region) -- the host never learns them.
+  const uint32_t* ctrl;
+  const float2* in;
+  float2* out;
+  DevChan ctrl_ch, in_ch, out_ch;
+  int channel_mode;
+};
+
+__device__ __forceinline__ const uint32_t* io_ctrl(const DpdIO& io) {
+  return io.channel_mode ? reinterpret_cast<const uint32_t*>(chan_read_region(io.ctrl_ch)) : io.ctrl;
+}
+__device__ __forceinline__ const float2* io_in(const DpdIO& io) {
+  return io.channel_mode ? reinterpret_cast<const float2*>(chan_read_region(io.in_ch)) : io.in;
+}
+__device__ __forceinline__ float2* io_out(const DpdIO& io) {
+  return io.channel_mode ? reinterpret_cast<float2*>(chan_write_region(io.out_ch)) : io.out;
+}
+
+// poly_branch for one sample (dpd.cpp:67-73).
+__device__ __forceinline__ float2 poly_sample(float re, float im, int b) {
+  if (b == 1) return make_float2(re, im);  // scale 1.0f: re*1 == re exactly
+  const float mag = __fsqrt_rn(__fadd_rn(__fmul_rn(re, re), __fmul_rn(im, im)));
+  float scale = mag;  // 1.0f * mag == mag exactly
+  for (int p = 2; p < b; ++p) scale = __fmul_rn(scale, mag);
+  return make_float2(__fmul_rn(re, scale), __fmul_rn(im, scale));
+}
+
+// ---------------------------------------------------------------------------
+// Prep: per branch (one CTA each), scan the batch's control tokens, build
+// the compacted active-block list, emit the history table H[p][b][j] for
+// every active (p, b), and advance the carried FirState.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) dpd_prep_kernel(DpdIO io, const float2* state_in,
+                                                        float2* state_out, float2* hist,
+                                                        int* act, unsigned long long K,
+                                                        unsigned period, int T,
+                                                        unsigned* err) {
+  const int b = blockIdx.x + 1;
+  const uint32_t* ctrl = io_ctrl(io);
+  const float2* x = io_in(io);
+  int* my_act = act + (size_t)blockIdx.x * K;
+  __shared__ float2 old_state[kMaxTaps];
+  __shared__ unsigned warp_counts[32];
+  __shared__ unsigned long long total;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  if (tid < T - 1) old_state[tid] = state_in[(size_t)blockIdx.x * (kMaxTaps - 1) + tid];
+  if (tid == 0) total = 0;
+  __syncthreads();
+
+  // Compaction of { p : bit b-1 of ctrl[p] } with warp ballots.
+  for (unsigned long long base = 0; base < K; base += blockDim.x) {
+    const unsigned long long p = base + tid;
+    uint32_t m = p < K ? ctrl[p] : 0;
+    if (b == 1 && p < K && (m >> kBranches)) atomicCAS(err, 0u, (unsigned)DF_ECONTROL);
+    const bool on = (m >> (b - 1)) & 1u;
+    const unsigned ballot = __ballot_sync(0xffffffffu, on);
+    if (lane == 0) warp_counts[warp] = __popc(ballot);
+    __syncthreads();
+    if (warp == 0) {
+      unsigned v = lane < nwarps ? warp_counts[lane] : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        unsigned n = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += n;
+      }
+      if (lane < nwarps) warp_counts[lane] = v;  // inclusive
+    }
+    __syncthreads();
+    const unsigned before = (warp ? warp_counts[warp - 1] : 0) + __popc(ballot & ((1u << lane) - 1));
+    if (on) my_act[total + before] = (int)p;
+    __syncthreads();
+    if (tid == 0) total += warp_counts[nwarps - 1];
+    __syncthreads();
+  }
+  const unsigned long long C = total;
+  const int H1 = T - 1;
+
+  // History table: entry (c, j) for the c-th active block of this branch.
+  // Position of x[-(j+1)] in the branch's active stream: c*period - (j+1).
+  const unsigned long long items = C * (unsigned long long)H1;
+  for (unsigned long long it = tid; it < items; it += blockDim.x) {
+    const unsigned long long c = it / H1;
+    const int j = (int)(it % H1);
+    const long long pos = (long long)(c * period) - (j + 1);
+    float2 u;
+    if (pos >= 0) {
+      const int q = my_act[pos / period];
+      const float2 v = x[(size_t)q * period + (size_t)(pos % period)];
+      u = poly_sample(v.x, v.y, b);
+    } else {
+      u = old_state[-pos - 1];
+    }
+    const int p = my_act[c];
+    hist[((size_t)p * kBranches + blockIdx.x) * H1 + j] = u;
+  }
+  // New FirState = history at the end of the batch (unchanged if C == 0).
+  __syncthreads();
+  if (tid < H1 && C > 0) {
+    const long long pos = (long long)(C * period) - (tid + 1);
+    float2 u;
+    if (pos >= 0) {
+      const int q = my_act[pos / period];
+      const float2 v = x[(size_t)q * period + (size_t)(pos % period)];
+      u = poly_sample(v.x, v.y, b);
+    } else {
+      u = old_state[-pos - 1];
+    }
+    state_out[(size_t)blockIdx.x * (kMaxTaps - 1) + tid] = u;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Main: one CTA = one tile of S = THREADS*V samples of one block.  Per
+// active branch: poly of the tile window into smem, then a register-blocked
+// FIR (V consecutive outputs per thread, sliding window over the taps), and
+// the branch sum in registers.
+// ---------------------------------------------------------------------------
+__host__ __device__ constexpr int pad_index(int w) { return w + (w >> 3); }  // bank-conflict pad
+
+template <int T, int V, int THREADS>
+struct MainCfg {
+  static constexpr int S = THREADS * V;             // samples per tile
+  static constexpr int W = S + T - 1;               // window incl. history
+  static constexpr int WP = pad_index(W) + 1;       // padded window length
+  static constexpr int M = (W + THREADS - 1) / THREADS;  // poly positions per thread
+};
+
+template <int T, int V, int THREADS>
+__global__ void __launch_bounds__(THREADS) dpd_main_kernel(DpdIO io, const float2* __restrict__ taps_g,
+                                                            const float2* __restrict__ hist,
+                                                            unsigned period, unsigned tiles_per_block,
+                                                            unsigned* err, unsigned* done_counter) {
+  using C = MainCfg<T, V, THREADS>;
+  constexpr int H1 = T - 1;
+  __shared__ float2 taps_s[kBranches * T];
+  __shared__ float2 us[2][C::WP];
+
+  const unsigned long long p = blockIdx.y;
+  const unsigned tile = blockIdx.x;
+  const uint32_t* ctrl = io_ctrl(io);
+  const float2* __restrict__ x = io_in(io);
+  float2* __restrict__ y = io_out(io);
+
+  const int tid = threadIdx.x;
+  const unsigned t0 = tile * C::S;
+  const int n = (int)min((unsigned)C::S, period - t0);  // valid outputs in this tile
+  const size_t blk = (size_t)p * period;
+  uint32_t mask = ctrl[p];
+  if (mask >> kBranches) {
+    if (tid == 0) atomicCAS(err, 0u, (unsigned)DF_ECONTROL);
+    mask &= (1u << kBranches) - 1;
+  }
+
+  for (int i = tid; i < kBranches * T; i += THREADS) taps_s[i] = taps_g[i];
+
+  // Window position w in [0, W): sample index t0 - (T-1) + w of the block.
+  // Each thread owns positions w = tid + m*THREADS; keeps x, mag, scale.
+  float xr[C::M], xi[C::M], mg[C::M], sc[C::M];
+#pragma unroll
+  for (int m = 0; m < C::M; ++m) {
+    const int w = tid + m * THREADS;
+    const long long s = (long long)t0 - H1 + w;
+    float2 v = make_float2(0.f, 0.f);
+    if (w < n + H1 && s >= 0) v = x[blk + s];
+    xr[m] = v.x;
+    xi[m] = v.y;
+    mg[m] = __fsqrt_rn(__fadd_rn(__fmul_rn(v.x, v.x), __fmul_rn(v.y, v.y)));
+    sc[m] = 1.0f;
+  }
+
+  float outr[V], outi[V];
+  bool first_branch = true;
+  int prev_b = 1;
+  int buf = 0;
+#pragma unroll 1
+  for (uint32_t bits = mask; bits; bits &= bits - 1) {
+    const int b = __ffs(bits);  // ascending branch order
+    // scale_b = scale_{prev}*mag^(b-prev): the reference's repeated product.
+#pragma unroll
+    for (int m = 0; m < C::M; ++m) {
+      for (int q = prev_b; q < b; ++q) sc[m] = (q == 1) ? mg[m] : __fmul_rn(sc[m], mg[m]);
+    }
+    prev_b = b;
+    float2* u = us[buf];
+#pragma unroll
+    for (int m = 0; m < C::M; ++m) {
+      const int w = tid + m * THREADS;
+      if (w < C::W) {
+        const long long s = (long long)t0 - H1 + w;
+        float2 v;
+        if (s < 0) {
+          v = hist[((size_t)p * kBranches + (b - 1)) * H1 + (size_t)(-s - 1)];
+        } else if (b == 1) {
+          v = make_float2(xr[m], xi[m]);
+        } else {
+          v = make_float2(__fmul_rn(xr[m], sc[m]), __fmul_rn(xi[m], sc[m]));
+        }
+        u[pad_index(w)] = v;
+      }
+    }
+    __syncthreads();
+
+    // FIR over outputs o = tid*V + j (window index o + k' with k' = T-1-k).
+    const float2* tb = taps_s + (b - 1) * T;
+    float ar[V], ai[V], wr[V], wi[V];
+    const int o0 = tid * V;
+    // Window for tap k = 0: u[o0 + H1 + j].
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      const float2 v = u[pad_index(o0 + H1 + j)];
+      wr[j] = v.x;
+      wi[j] = v.y;
+    }
+    {
+      const float2 t = tb[0];
+#pragma unroll
+      for (int j = 0; j < V; ++j) {  // tap 0 without the leading 0.0f +
+        ar[j] = __fsub_rn(__fmul_rn(t.x, wr[j]), __fmul_rn(t.y, wi[j]));
+        ai[j] = __fadd_rn(__fmul_rn(t.x, wi[j]), __fmul_rn(t.y, wr[j]));
+      }
+    }
+#pragma unroll
+    for (int k = 1; k < T; ++k) {
+      // Slide: window for tap k is u[o0 + H1 - k + j].
+#pragma unroll
+      for (int j = V - 1; j > 0; --j) {
+        wr[j] = wr[j - 1];
+        wi[j] = wi[j - 1];
+      }
+      const float2 v = u[pad_index(o0 + H1 - k)];
+      wr[0] = v.x;
+      wi[0] = v.y;
+      const float2 t = tb[k];
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        ar[j] = __fadd_rn(ar[j], __fsub_rn(__fmul_rn(t.x, wr[j]), __fmul_rn(t.y, wi[j])));
+        ai[j] = __fadd_rn(ai[j], __fadd_rn(__fmul_rn(t.x, wi[j]), __fmul_rn(t.y, wr[j])));
+      }
+    }
+    if (first_branch) {
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        outr[j] = ar[j];
+        outi[j] = ai[j];
+      }
+      first_branch = false;
+    } else {
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        outr[j] = __fadd_rn(outr[j], ar[j]);
+        outi[j] = __fadd_rn(outi[j], ai[j]);
+      }
+    }
+    buf ^= 1;
+  }
+  if (first_branch) {  // no active branch: the adder emits +0.0f
+#pragma unroll
+    for (int j = 0; j < V; ++j) outr[j] = outi[j] = 0.0f;
+  }
+
+  // Stage through smem for coalesced stores (reuse the idle buffer).
+  __syncthreads();
+  float2* st = us[buf];
+#pragma unroll
+  for (int j = 0; j < V; ++j)
+    st[pad_index(tid * V + j)] = make_float2(__fadd_rn(outr[j], 0.0f), __fadd_rn(outi[j], 0.0f));
+  __syncthreads();
+  for (int o = tid; o < n; o += THREADS) y[blk + t0 + o] = st[pad_index(o)];
+
+  if (io.channel_mode) {
+    // Last CTA commits the firing batch: K control tokens, K block tokens
+    // consumed, K block tokens produced (all ports always at full rate).
+    __shared__ bool last;
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      const unsigned total = gridDim.x * gridDim.y;
+      last = atomicAdd(done_counter, 1u) == total - 1;
+    }
+    __syncthreads();
+    if (last && tid == 0) {
+      __threadfence();
+      *done_counter = 0;
+      chan_commit_read(io.ctrl_ch, io.ctrl_ch.rate);
+      chan_commit_read(io.in_ch, io.in_ch.rate);
+      chan_commit_write(io.out_ch, io.out_ch.rate);
+    }
+  }
+}
+
+// Generic-T fallback (T not 10/32): simple per-output loop, same op order.
+__global__ void dpd_main_generic_kernel(DpdIO io, const float2* __restrict__ taps_g,
+                                        const float2* __restrict__ hist, unsigned period, int T,
+                                        unsigned* err, unsigned* done_counter) {
+  const unsigned long long p = blockIdx.y;
+  const uint32_t* ctrl = io_ctrl(io);
+  const float2* x = io_in(io);
+  float2* y = io_out(io);
+  uint32_t mask = ctrl[p];
+  if (mask >> kBranches) {
+    if (threadIdx.x == 0) atomicCAS(err, 0u, (unsigned)DF_ECONTROL);
+    mask &= (1u << kBranches) - 1;
+  }
+  const int H1 = T - 1;
+  const size_t blk = (size_t)p * period;
+  for (unsigned o = blockIdx.x * blockDim.x + threadIdx.x; o < period; o += gridDim.x * blockDim.x) {
+    float outr = 0.0f, outi = 0.0f;
+    for (uint32_t bits = mask; bits; bits &= bits - 1) {
+      const int b = __ffs(bits);
+      float ar = 0.0f, ai = 0.0f;
+      for (int k = 0; k < T; ++k) {
+        const long long s = (long long)o - k;
+        float2 u;
+        if (s >= 0) {
+          const float2 v = x[blk + s];
+          u = poly_sample(v.x, v.y, b);
+        } else {
+          u = hist[((size_t)p * kBranches + (b - 1)) * H1 + (size_t)(-s - 1)];
+        }
+        const float2 t = taps_g[(b - 1) * T + k];
+        ar = __fadd_rn(ar, __fsub_rn(__fmul_rn(t.x, u.x), __fmul_rn(t.y, u.y)));
+        ai = __fadd_rn(ai, __fadd_rn(__fmul_rn(t.x, u.y), __fmul_rn(t.y, u.x)));
+      }
+      outr = __fadd_rn(outr, ar);
+      outi = __fadd_rn(outi, ai);
+    }
+    y[blk + o] = make_float2(outr, outi);
+  }
+  if (io.channel_mode) {
+    __shared__ bool last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      last = atomicAdd(done_counter, 1u) == gridDim.x * gridDim.y - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+      __threadfence();
+      *done_counter = 0;
+      chan_commit_read(io.ctrl_ch, io.ctrl_ch.rate);
+      chan_commit_read(io.in_ch, io.in_ch.rate);
+      chan_commit_write(io.out_ch, io.out_ch.rate);
+    }
+  }
+}
+
+__global__ void dpd_config_kernel(const uint16_t* __restrict__ sched, unsigned len,
+                                  unsigned long long first, unsigned long long count,
+                                  uint32_t* __restrict__ ctrl) {
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < count;
+       i += (unsigned long long)gridDim.x * blockDim.x)
+    ctrl[i] = sched[(first + i) % len];  // LE 4-byte wire form (dpd.hpp:38-41)
+}
+
+constexpr int kV = 8;
+constexpr int kThreads = 128;
+
+}  // namespace
+}  // namespace df
+
+using namespace df;
+
+struct df_dpd {
+  int device = 0;
+  uint32_t period = 0;
+  uint32_t T = 10;
+  float2* taps = nullptr;      // device, 10*T
+  float2* state = nullptr;     // device, 10*(kMaxTaps-1): FirState per branch
+  unsigned* scratch = nullptr; // [0] error word, [1] done counter
+  float2* hist = nullptr;      // device history table, capacity hist_blocks
+  int* act = nullptr;          // device active lists, 10*hist_blocks
+  unsigned long long hist_blocks = 0;
+  // run_host resources
+  void* ctrl_buf = nullptr;
+  unsigned long long ctrl_cap = 0;
+  uint16_t* sched_dev = nullptr;
+  size_t sched_cap = 0;
+};
+
+namespace {
+
+int ensure_hist(df_dpd* d, unsigned long long K) {
+  if (K <= d->hist_blocks) return DF_OK;
+  unsigned long long cap = std::max<unsigned long long>(K, 64);
+  cudaFree(d->hist);
+  cudaFree(d->act);
+  d->hist = nullptr;
+  d->act = nullptr;
+  d->hist_blocks = 0;
+  const size_t H1 = std::max<uint32_t>(d->T - 1, 1);
+  DF_CHECK_CUDA(cudaMalloc(&d->hist, cap * kBranches * H1 * sizeof(float2)));
+  DF_CHECK_CUDA(cudaMalloc(&d->act, cap * kBranches * sizeof(int)));
+  d->hist_blocks = cap;
+  return DF_OK;
+}
+
+int launch_dpd(df_dpd* d, const DpdIO& io, unsigned long long K, cudaStream_t s) {
+  if (K == 0) return DF_OK;
+  DF_REQUIRE(K <= 0x7fffffffull / 2, DF_EINVAL, "dpd: batch of %llu blocks too large", K);
+  DF_TRY(ensure_hist(d, K));
+  unsigned* err = d->scratch;
+  unsigned* done = d->scratch + 1;
+  if (d->T > 1) {
+    dpd_prep_kernel<<<kBranches, 1024, 0, s>>>(io, d->state, d->state, d->hist, d->act, K, d->period,
+                                                (int)d->T, err);
+    DF_TRY(after_launch("dpd_prep_kernel"));
+  }
+  if (d->T == 10 || d->T == 32) {
+    constexpr int S = kThreads * kV;
+    const unsigned tiles = (d->period + S - 1) / S;
+    DF_REQUIRE(K <= 65535u * 1024u, DF_EINVAL, "dpd: batch too large");
+    // blockIdx.y indexes blocks: split very large batches into launches.
+    for (unsigned long long base = 0; base < K; base += 65535) {
+      const unsigned long long k = std::min<unsigned long long>(65535, K - base);
+      DpdIO sub = io;
+      if (!io.channel_mode) {
+        sub.ctrl = io.ctrl + base;
+        sub.in = io.in + base * d->period;
+        sub.out = io.out + base * d->period;
+      } else {
+        DF_REQUIRE(K <= 65535, DF_EINVAL, "dpd: channel firing batch > 65535");
+      }
+      const float2* hist = d->hist + base * kBranches * (d->T - 1);
+      dim3 grid(tiles, (unsigned)k);
+      if (d->T == 10)
+        dpd_main_kernel<10, kV, kThreads><<<grid, kThreads, 0, s>>>(sub, d->taps, hist, d->period, tiles, err, done);
+      else
+        dpd_main_kernel<32, kV, kThreads><<<grid, kThreads, 0, s>>>(sub, d->taps, hist, d->period, tiles, err, done);
+      DF_TRY(after_launch("dpd_main_kernel"));
+    }
+  } else {
+    for (unsigned long long base = 0; base < K; base += 65535) {
+      const unsigned long long k = std::min<unsigned long long>(65535, K - base);
+      DpdIO sub = io;
+      if (!io.channel_mode) {
+        sub.ctrl = io.ctrl + base;
+        sub.in = io.in + base * d->period;
+        sub.out = io.out + base * d->period;
+      }
+      const float2* hist = d->hist + base * kBranches * std::max<uint32_t>(d->T - 1, 1);
+      dim3 grid(std::min<unsigned>((d->period + 255) / 256, 64), (unsigned)k);
+      dpd_main_generic_kernel<<<grid, 256, 0, s>>>(sub, d->taps, hist, d->period, (int)d->T, err, done);
+      DF_TRY(after_launch("dpd_main_generic_kernel"));
+    }
+  }
+  return DF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int df_dpd_create(int device, uint32_t period, uint32_t T, const float* taps_host, df_dpd** out) {
+  DF_REQUIRE(out, DF_EINVAL, "df_dpd_create: null out pointer");
+  *out = nullptr;
+  DF_REQUIRE(period >= 1, DF_EINVAL, "dpd: period must be >= 1");  // dpd.cpp:152-154
+  DF_REQUIRE(T >= 1 && T <= kMaxTaps, DF_EINVAL, "dpd: taps per branch %u outside [1,%d]", T, kMaxTaps);
+  DF_REQUIRE(taps_host, DF_EINVAL, "dpd: null taps");
+  DF_CHECK_CUDA(cudaSetDevice(device));
+  auto* d = new df_dpd();
+  d->device = device;
+  d->period = period;
+  d->T = T;
+  cudaError_t e = cudaMalloc(&d->taps, sizeof(float2) * kBranches * T);
+  if (e == cudaSuccess) e = cudaMalloc(&d->state, sizeof(float2) * kBranches * (kMaxTaps - 1));
+  if (e == cudaSuccess) e = cudaMalloc(&d->scratch, 64);
+  if (e == cudaSuccess) e = cudaMemcpy(d->taps, taps_host, sizeof(float2) * kBranches * T, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemset(d->state, 0, sizeof(float2) * kBranches * (kMaxTaps - 1));
+  if (e == cudaSuccess) e = cudaMemset(d->scratch, 0, 64);
+  if (e != cudaSuccess) {
+    int rc = cuda_status(e, "df_dpd_create");
+    cudaFree(d->taps);
+    cudaFree(d->state);
+    cudaFree(d->scratch);
+    delete d;
+    return rc;
+  }
+  *out = d;
+  return DF_OK;
+}
+
+int df_dpd_destroy(df_dpd* d) {
+  if (!d) return DF_OK;
+  cudaSetDevice(d->device);
+  cudaFree(d->taps);
+  cudaFree(d->state);
+  cudaFree(d->scratch);
+  cudaFree(d->hist);
+  cudaFree(d->act);
+  cudaFree(d->ctrl_buf);
+  cudaFree(d->sched_dev);
+  delete d;
+  return DF_OK;
+}
+
+int df_dpd_set_taps(df_dpd* d, const float* taps_host, void* stream) {
+  DF_REQUIRE(d && taps_host, DF_EINVAL, "df_dpd_set_taps: null argument");
+  DF_CHECK_CUDA(cudaSetDevice(d->device));
+  DF_CHECK_CUDA(cudaMemcpyAsync(d->taps, taps_host, sizeof(float2) * kBranches * d->T,
+                                cudaMemcpyHostToDevice, as_stream(stream)));
+  DF_CHECK_CUDA(cudaStreamSynchronize(as_stream(stream)));
+  return DF_OK;
+}
+
+int df_dpd_reset(df_dpd* d, void* stream) {
+  DF_REQUIRE(d, DF_EINVAL, "df_dpd_reset: null actor");
+  DF_CHECK_CUDA(cudaSetDevice(d->device));
+  DF_CHECK_CUDA(cudaMemsetAsync(d->state, 0, sizeof(float2) * kBranches * (kMaxTaps - 1), as_stream(stream)));
+  DF_CHECK_CUDA(cudaMemsetAsync(d->scratch, 0, 64, as_stream(stream)));
+  return DF_OK;
+}
+
+int df_dpd_get_state(df_dpd* d, float* state_host) {
+  DF_REQUIRE(d && state_host, DF_EINVAL, "df_dpd_get_state: null argument");
+  DF_CHECK_CUDA(cudaSetDevice(d->device));
+  DF_CHECK_CUDA(cudaDeviceSynchronize());
+  std::vector<float2> st((size_t)kBranches * (kMaxTaps - 1));
+  DF_CHECK_CUDA(cudaMemcpy(st.data(), d->state, st.size() * sizeof(float2), cudaMemcpyDeviceToHost));
+  const uint32_t H1 = d->T - 1;
+  for (int b = 0; b < kBranches; ++b)
+    for (uint32_t j = 0; j < H1; ++j) {
+      state_host[2 * (b * H1 + j)] = st[b * (kMaxTaps - 1) + j].x;
+      state_host[2 * (b * H1 + j) + 1] = st[b * (kMaxTaps - 1) + j].y;
+    }
+  return DF_OK;
+}
+
+int df_dpd_error(df_dpd* d) {
+  DF_REQUIRE(d, DF_EINVAL, "df_dpd_error: null actor");
+  DF_CHECK_CUDA(cudaSetDevice(d->device));
+  DF_CHECK_CUDA(cudaDeviceSynchronize());
+  unsigned err = 0;
+  DF_CHECK_CUDA(cudaMemcpy(&err, d->scratch, sizeof err, cudaMemcpyDeviceToHost));
+  if (err == DF_ECONTROL) return set_error(DF_ECONTROL, "config token names a branch beyond 10");
+  if (err) return set_error((int)err, "dpd: device error %u", err);
+  return DF_OK;
+}
+
+int df_dpd_fire(df_dpd* d, const uint32_t* ctrl_dev, const float* in_dev, float* out_dev,
+                uint64_t blocks, void* stream) {
+  DF_REQUIRE(d, DF_EINVAL, "df_dpd_fire: null actor");
+  if (blocks == 0) return DF_OK;
+  DF_REQUIRE(ctrl_dev && in_dev && out_dev, DF_EINVAL, "df_dpd_fire: null buffer");
+  DF_REQUIRE(in_dev != out_dev, DF_EINVAL, "df_dpd_fire: in-place firing is not supported");
+  DF_CHECK_CUDA(cudaSetDevice(d->device));
+  DpdIO io{};
+  io.ctrl = ctrl_dev;
+  io.in = reinterpret_cast<const float2*>(in_dev);
+  io.out = reinterpret_cast<float2*>(out_dev);
+  io.channel_mode = 0;
+  return launch_dpd(d, io, blocks, as_stream(stream));
+}
+
+int df_dpd_fire_channels(df_dpd* d, df_channel* ctrl, df_channel* in, df_channel* out,
+                         uint32_t firings, void* stream) {
+  DF_REQUIRE(d && ctrl && in && out, DF_EINVAL, "df_dpd_fire_channels: null argument");
+  if (firings == 0) return DF_OK;
+  DF_REQUIRE(ctrl->token_size == 4 && ctrl->rate == firings, DF_ELOGIC,
+             "dpd: control channel must carry 4-byte tokens at rate %u", firings);
+  DF_REQUIRE(in->token_size == (size_t)d->period * 8 && in->rate == firings, DF_ELOGIC,
+             "dpd: input channel token must be one period (%u samples) at rate %u", d->period, firings);
+  DF_REQUIRE(out->token_size == (size_t)d->period * 8 && out->rate == firings, DF_ELOGIC,
+             "dpd: output channel token must be one period at rate %u", firings);
+  DF_REQUIRE(!ctrl->has_delay, DF_ELOGIC, "delay token on a channel into a control port");
+  for (df_channel* c : {ctrl, in}) {
+    DF_REQUIRE(c->reader != Endpoint::host, DF_ELOGIC, "dpd: input endpoint is host-driven");
+    c->reader = Endpoint::device;
+  }
+  DF_REQUIRE(out->writer != Endpoint::host, DF_ELOGIC, "dpd: output endpoint is host-driven");
+  out->writer = Endpoint::device;
+  DF_CHECK_CUDA(cudaSetDevice(d->device));
+  DpdIO io{};
+  io.channel_mode = 1;
+  io.ctrl_ch = ctrl->dev();
+  io.in_ch = in->dev();
+  io.out_ch = out->dev();
+  return launch_dpd(d, io, firings, as_stream(stream));
+}
+
+int df_dpd_config_tokens(int device, const uint16_t* schedule_host, size_t len, uint64_t first,
+                         uint64_t count, uint32_t* ctrl_dev, void* stream) {
+  DF_REQUIRE(schedule_host && len > 0, DF_EINVAL, "dpd: schedule must not be empty");
+  if (count == 0) return DF_OK;
+  DF_CHECK_CUDA(cudaSetDevice(device));
+  uint16_t* sd = nullptr;
+  DF_CHECK_CUDA(cudaMallocAsync(&sd, len * sizeof(uint16_t), as_stream(stream)));
+  DF_CHECK_CUDA(cudaMemcpyAsync(sd, schedule_host, len * sizeof(uint16_t), cudaMemcpyHostToDevice,
+                                as_stream(stream)));
+  const unsigned blocks = (unsigned)std::min<uint64_t>((count + 255) / 256, 1184);
+  dpd_config_kernel<<<blocks, 256, 0, as_stream(stream)>>>(sd, (unsigned)len, first, count, ctrl_dev);
+  int rc = after_launch("dpd_config_kernel");
+  DF_CHECK_CUDA(cudaFreeAsync(sd, as_stream(stream)));
+  return rc;
+}
+
+int df_dpd_run_host(df_dpd* d, const float* in_host, float* out_host, uint64_t samples,
+                    const uint16_t* schedule_host, size_t schedule_len, uint64_t chunk_blocks,
+                    void* stream) {
+  DF_REQUIRE(d && in_host && out_host, DF_EINVAL, "df_dpd_run_host: null argument");
+  DF_REQUIRE(schedule_host && schedule_len > 0, DF_EINVAL, "dpd: schedule must not be empty");
+  DF_REQUIRE(samples % d->period == 0, DF_EINVAL,
+             "dpd: sample count must be a nonzero multiple of the period");
+  if (samples == 0) return DF_OK;
+  DF_CHECK_CUDA(cudaSetDevice(d->device));
+  const uint64_t blocks = samples / d->period;
+  if (chunk_blocks == 0) chunk_blocks = std::max<uint64_t>(1, (64ull << 20) / (8ull * d->period));
+  chunk_blocks = std::min(chunk_blocks, blocks);
+  const size_t chunk_bytes = chunk_blocks * d->period * 8ull;
+  cudaStream_t cs = as_stream(stream);
+  // Two slots of (in, out) buffers; copies on dedicated streams.
+  float* bin[2] = {nullptr, nullptr};
+  float* bout[2] = {nullptr, nullptr};
+  uint32_t* ctrl = nullptr;
+  uint16_t* sd = nullptr;
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t in_ready[2], comp_done[2], out_free[2];
+  int rc = DF_OK;
+  auto ck = [&](cudaError_t e, const char* w) {
+    if (rc == DF_OK && e != cudaSuccess) rc = cuda_status(e, w);
+    return rc == DF_OK;
+  };
+  ck(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking), "stream");
+  ck(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking), "stream");
+  for (int i = 0; i < 2; ++i) {
+    ck(cudaMalloc(&bin[i], chunk_bytes), "cudaMalloc");
+    ck(cudaMalloc(&bout[i], chunk_bytes), "cudaMalloc");
+    ck(cudaEventCreateWithFlags(&in_ready[i], cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&comp_done[i], cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&out_free[i], cudaEventDisableTiming), "event");
+  }
+  ck(cudaMalloc(&ctrl, blocks * sizeof(uint32_t)), "cudaMalloc");
+  ck(cudaMalloc(&sd, schedule_len * sizeof(uint16_t)), "cudaMalloc");
+  ck(cudaMemcpyAsync(sd, schedule_host, schedule_len * sizeof(uint16_t), cudaMemcpyHostToDevice, cs), "copy");
+  if (rc == DF_OK) {
+    // Config actor: one control token per block, on device.
+    dpd_config_kernel<<<(unsigned)std::min<uint64_t>((blocks + 255) / 256, 1184), 256, 0, cs>>>(
+        sd, (unsigned)schedule_len, 0, blocks, ctrl);
+    rc = after_launch("dpd_config_kernel");
+  }
+  // Slot reuse ordering: in slot i is free once compute of chunk c-2 is
+  // done (comp_done); out slot i is free once its D2H is done (out_free).
+  const uint64_t nchunks = (blocks + chunk_blocks - 1) / chunk_blocks;
+  for (uint64_t c = 0; c < nchunks && rc == DF_OK; ++c) {
+    const int i = (int)(c & 1);
+    const uint64_t b0 = c * chunk_blocks;
+    const uint64_t nb = std::min(chunk_blocks, blocks - b0);
+    const size_t bytes = nb * d->period * 8ull;
+    if (c >= 2) ck(cudaStreamWaitEvent(h2d, comp_done[i], 0), "wait");
+    ck(cudaMemcpyAsync(bin[i], in_host + 2 * b0 * d->period, bytes, cudaMemcpyHostToDevice, h2d), "h2d");
+    ck(cudaEventRecord(in_ready[i], h2d), "record");
+    ck(cudaStreamWaitEvent(cs, in_ready[i], 0), "wait");
+    if (c >= 2) ck(cudaStreamWaitEvent(cs, out_free[i], 0), "wait");
+    if (rc != DF_OK) break;
+    DpdIO io{};
+    io.ctrl = ctrl + b0;
+    io.in = reinterpret_cast<const float2*>(bin[i]);
+    io.out = reinterpret_cast<float2*>(bout[i]);
+    rc = launch_dpd(d, io, nb, cs);
+    ck(cudaEventRecord(comp_done[i], cs), "record");
+    ck(cudaStreamWaitEvent(d2h, comp_done[i], 0), "wait");
+    ck(cudaMemcpyAsync(out_host + 2 * b0 * d->period, bout[i], bytes, cudaMemcpyDeviceToHost, d2h), "d2h");
+    ck(cudaEventRecord(out_free[i], d2h), "record");
+  }
+  ck(cudaStreamSynchronize(d2h), "sync");
+  ck(cudaStreamSynchronize(cs), "sync");
+  for (int i = 0; i < 2; ++i) {
+    cudaFree(bin[i]);
+    cudaFree(bout[i]);
+    cudaEventDestroy(in_ready[i]);
+    cudaEventDestroy(comp_done[i]);
+    cudaEventDestroy(out_free[i]);
+  }
+  cudaFree(ctrl);
+  cudaFree(sd);
+  if (h2d) cudaStreamDestroy(h2d);
+  if (d2h) cudaStreamDestroy(d2h);
+  return rc;
+}
+
+}  // extern "C"

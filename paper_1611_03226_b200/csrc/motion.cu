@@ -1,0 +1,738 @@
+// motion.cu -- the motion-detection actor chain on sm_100a.
+//
+// Replaces the reference's gauss -> thres -> med actors
+// (proj/src/motion.cpp:144-176) and their kernels gauss5x5 / thres_diff /
+// median5 (:27-74) with ONE fused kernel per firing; the gauss -> thres
+// "prev" channel with its delay token (:131, :153) becomes a gauss frame
+// carried on chip between consecutive frames and, between firings, a
+// device-resident delay token.  Extension: RGB input converted in the same
+// kernel (gray = (77R + 150G + 29B + 128) >> 8, BT.601 integer luma).
+//
+// Byte-exact arithmetic, packed SIMD (HBM-bound target: 4 B/px):
+//   gray   6 x IDP.4A per 4 px (weights 77/150/29, +128 in the accumulator)
+//   gauss  horizontal 5-tap [1 4 6 4 1] with IDP.4A on the packed gray
+//          bytes (2 per px), vertical on 16x2 packed lanes (max 65408 <
+//          2^16, +128 folded into the first add), (acc+128)>>8 by byte
+//          selection -- identical to motion.cpp:38-45 for every pixel
+//   thres  VABSDIFF4, then a SWAR byte compare d > thr (exact for all thr)
+//   median the thresholded map is binary, so the plus-shaped median of 5
+//          (motion.cpp:68-71) is a bitwise majority-of-5 on byte lanes
+//   out    0/255 bytes by PRMT sign replication
+// Borders follow the reference exactly: gauss copies gray for the 2-px
+// frame border (:34-37), median copies the threshold map for the 1-px
+// border (:64-67), thres runs everywhere.
+//
+// Work decomposition: one warp owns a column tile (32 lanes x 8 px, lanes
+// 1..30 produce output, lanes 0/31 are the horizontal halo) of a band of
+// R rows, and walks a range of frames (temporal walk): gauss(prev) for its
+// band lives in shared memory, so every input byte is read once per frame
+// (+ vertical/horizontal halo re-reads, which hit L2).  Frame ranges that do
+// not start the firing recompute gauss(f0-1) once.  No __syncthreads: warps
+// are independent; neighbours are exchanged with shuffles.
+#include <algorithm>
+#include <cstring>
+
+#include "channel_dev.cuh"
+#include "channel_host.hpp"
+#include "common.cuh"
+
+namespace df {
+namespace {
+
+constexpr int kBandRows = 32;             // R
+constexpr int kWarpsPerCta = 4;
+constexpr int kPxPerLane = 8;
+constexpr int kOutPxPerWarp = 30 * kPxPerLane;  // 240
+
+struct MotionIO {
+  const unsigned char* in;      // frames (raw mode)
+  unsigned char* out;
+  const unsigned char* prev;    // delay token in (gauss frame)
+  unsigned char* next;          // delay token out (gauss frame)
+  unsigned char* next_copy;     // Fig. 2 phase-2 duplicate (slot 0) or null
+  DevChan in_ch, out_ch, delay_ch;
+  int channel_mode;
+};
+
+struct MotionGeom {
+  int W, H;
+  int frames;        // frames in this firing
+  int chunk;         // frames per temporal chunk
+  unsigned thr_k;    // SWAR constant
+  unsigned thr_sel;  // 0xFFFFFFFF if thr <= 127 else 0
+};
+
+__device__ __forceinline__ unsigned dp4a(unsigned a, unsigned b, unsigned c) {
+  return __dp4a(a, b, c);
+}
+__device__ __forceinline__ unsigned prmt(unsigned a, unsigned b, unsigned s) {
+  unsigned d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(s));
+  return d;
+}
+__device__ __forceinline__ unsigned lop_maj(unsigned a, unsigned b, unsigned c) {
+  unsigned d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xE8;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+__device__ __forceinline__ unsigned lop_or3(unsigned a, unsigned b, unsigned c) {
+  unsigned d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xFE;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+__device__ __forceinline__ unsigned lop_and3(unsigned a, unsigned b, unsigned c) {
+  unsigned d;
+  asm("lop3.b32 %0, %1, %2, %3, 0x80;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+// s ? a : b  (bitwise select)
+__device__ __forceinline__ unsigned lop_sel(unsigned s, unsigned a, unsigned b) {
+  unsigned d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xE2;" : "=r"(d) : "r"(a), "r"(s), "r"(b));
+  return d;
+}
+
+constexpr unsigned W8(unsigned a, unsigned b, unsigned c, unsigned d) {
+  return a | (b << 8) | (c << 16) | (d << 24);
+}
+
+// 4 gray bytes from 12 interleaved RGB bytes (w0,w1,w2 little endian).
+__device__ __forceinline__ unsigned rgb4_to_gray(unsigned w0, unsigned w1, unsigned w2) {
+  const unsigned r0 = dp4a(w0, W8(77, 150, 29, 0), 128u);
+  const unsigned r1 = dp4a(w1, W8(150, 29, 0, 0), dp4a(w0, W8(0, 0, 0, 77), 128u));
+  const unsigned r2 = dp4a(w2, W8(29, 0, 0, 0), dp4a(w1, W8(0, 0, 77, 150), 128u));
+  const unsigned r3 = dp4a(w2, W8(0, 77, 150, 29), 128u);
+  const unsigned lo = prmt(r0, r1, 0x0051);  // bytes [r0.b1, r1.b1]
+  const unsigned hi = prmt(r2, r3, 0x0051);
+  return prmt(lo, hi, 0x5410);
+}
+
+// Horizontal [1 4 6 4 1] over 4 px of word C with neighbours L (left word)
+// and R (right word): two 16x2 packed pair words.
+__device__ __forceinline__ void hgauss4(unsigned L, unsigned C, unsigned R, unsigned& p01,
+                                        unsigned& p23) {
+  const unsigned h0 = dp4a(L, W8(0, 0, 1, 4), dp4a(C, W8(6, 4, 1, 0), 0u));
+  const unsigned h1 = dp4a(L, W8(0, 0, 0, 1), dp4a(C, W8(4, 6, 4, 1), 0u));
+  const unsigned h2 = dp4a(C, W8(1, 4, 6, 4), dp4a(R, W8(1, 0, 0, 0), 0u));
+  const unsigned h3 = dp4a(C, W8(0, 1, 4, 6), dp4a(R, W8(4, 1, 0, 0), 0u));
+  p01 = prmt(h0, h1, 0x5410);
+  p23 = prmt(h2, h3, 0x5410);
+}
+
+// Vertical [1 4 6 4 1] on 16x2 lanes with +128, returns packed sums.
+__device__ __forceinline__ unsigned vgauss(unsigned a, unsigned b, unsigned c, unsigned d,
+                                          unsigned e) {
+  const unsigned A = a + e + 0x00800080u;
+  const unsigned B = b + d;
+  return c * 6u + (B * 4u + A);
+}
+
+// |cur - prev| > thr per byte -> flag in bit 7 (other bits don't-care).
+__device__ __forceinline__ unsigned thres4(unsigned cur, unsigned prev, const MotionGeom& g) {
+  const unsigned d = __vabsdiffu4(cur, prev);
+  const unsigned t = (d & 0x7F7F7F7Fu) + g.thr_k;
+  return lop_maj(t, d, g.thr_sel);
+}
+
+// Majority of 5 (bitwise): centre c, up u, down d, left l, right r.
+__device__ __forceinline__ unsigned maj5(unsigned c, unsigned u, unsigned d, unsigned l,
+                                         unsigned r) {
+  const unsigned any3 = lop_or3(c, u, d);
+  const unsigned m3 = lop_maj(c, u, d);
+  const unsigned all3 = lop_and3(c, u, d);
+  const unsigned X = lop_sel(r, any3, m3);
+  const unsigned Y = lop_sel(r, m3, all3);
+  return lop_sel(l, X, Y);
+}
+
+// --- row I/O -----------------------------------------------------------
+// Loads the 8 gray px [x, x+8) of row y (zeros outside the frame).
+template <int FMT, bool FAST>
+__device__ __forceinline__ void load_gray8(const unsigned char* __restrict__ frame, int y, int x,
+                                           int W, int H, unsigned& g0, unsigned& g1) {
+  g0 = g1 = 0;
+  if (y < 0 || y >= H || x >= W || x + kPxPerLane <= 0) return;
+  if (FAST) {
+    if (FMT == DF_MOTION_RGB) {
+      const uint2* p = reinterpret_cast<const uint2*>(frame + ((size_t)y * W + x) * 3);
+      const uint2 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
+      g0 = rgb4_to_gray(a.x, a.y, b.x);
+      g1 = rgb4_to_gray(b.y, c.x, c.y);
+    } else {
+      const uint2 a = __ldg(reinterpret_cast<const uint2*>(frame + (size_t)y * W + x));
+      g0 = a.x;
+      g1 = a.y;
+    }
+  } else {
+    unsigned char px[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int xi = x + i;
+      if (xi >= 0 && xi < W) {
+        if (FMT == DF_MOTION_RGB) {
+          const unsigned char* q = frame + ((size_t)y * W + xi) * 3;
+          px[i] = (unsigned char)((77u * q[0] + 150u * q[1] + 29u * q[2] + 128u) >> 8);
+        } else {
+          px[i] = frame[(size_t)y * W + xi];
+        }
+      } else {
+        px[i] = 0;
+      }
+    }
+    g0 = W8(px[0], px[1], px[2], px[3]);
+    g1 = W8(px[4], px[5], px[6], px[7]);
+  }
+}
+
+template <bool FAST>
+__device__ __forceinline__ void load_bytes8(const unsigned char* __restrict__ plane, int y, int x,
+                                            int W, int H, unsigned& a0, unsigned& a1) {
+  a0 = a1 = 0;
+  if (y < 0 || y >= H || x >= W || x + kPxPerLane <= 0) return;
+  if (FAST) {
+    const uint2 a = *reinterpret_cast<const uint2*>(plane + (size_t)y * W + x);
+    a0 = a.x;
+    a1 = a.y;
+  } else {
+    unsigned char px[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int xi = x + i;
+      px[i] = (xi >= 0 && xi < W) ? plane[(size_t)y * W + xi] : 0;
+    }
+    a0 = W8(px[0], px[1], px[2], px[3]);
+    a1 = W8(px[4], px[5], px[6], px[7]);
+  }
+}
+
+template <bool FAST>
+__device__ __forceinline__ void store_bytes8(unsigned char* __restrict__ plane, int y, int x, int W,
+                                             unsigned a0, unsigned a1) {
+  if (FAST) {
+    *reinterpret_cast<uint2*>(plane + (size_t)y * W + x) = make_uint2(a0, a1);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int xi = x + i;
+      if (xi >= 0 && xi < W) plane[(size_t)y * W + xi] = (unsigned char)((i < 4 ? a0 : a1) >> (8 * (i & 3)));
+    }
+  }
+}
+
+// One row slot of the 5-row rolling window.
+struct RowSlot {
+  unsigned h[4];   // horizontal sums, 16x2 packed: px (0,1), (2,3), (4,5), (6,7)
+  unsigned g[2];   // gray words
+  unsigned t[2];   // threshold flags (bit 7 per byte) once computed
+};
+
+// Byte masks (0xFF per byte) of columns in the gauss border (x < 2 or
+// x >= W-2) and the median border (x == 0 or x == W-1).
+__device__ __forceinline__ void column_masks(int x, int W, unsigned gm[2], unsigned mm[2]) {
+#pragma unroll
+  for (int w = 0; w < 2; ++w) {
+    unsigned a = 0, b = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int xi = x + 4 * w + i;
+      if (xi < 2 || xi >= W - 2) a |= 0xFFu << (8 * i);
+      if (xi == 0 || xi == W - 1) b |= 0xFFu << (8 * i);
+    }
+    gm[w] = a;
+    mm[w] = b;
+  }
+}
+
+// Processes one frame for this warp's (tile, band).  MODE 0: gauss only,
+// into the prev buffer (warm-up of a frame range).  MODE 1: full chain.
+template <int FMT, bool FAST, int MODE>
+__device__ __forceinline__ void frame_pass(const unsigned char* __restrict__ frame,
+                                           unsigned char* __restrict__ out,
+                                           unsigned char* __restrict__ next_tok,
+                                           unsigned char* __restrict__ next_copy,
+                                           uint2* __restrict__ prev_s, const MotionGeom& g, int y0,
+                                           int x, int lane, const unsigned gm[2],
+                                           const unsigned mm[2]) {
+  const int W = g.W, H = g.H;
+  const bool out_lane = lane >= 1 && lane <= 30;
+  RowSlot s[5];
+  // Row gy's slot is s[(gy - (y0 - 3)) % 5].  Rows y0-3 .. y0+R+2.
+  const int gy_begin = y0 - 3, gy_end = min(y0 + kBandRows + 3, H + 3);
+
+  auto produce = [&](RowSlot& r, int gy) {
+    unsigned g0, g1;
+    load_gray8<FMT, FAST>(frame, gy, x, W, H, g0, g1);
+    const unsigned left = __shfl_up_sync(0xffffffffu, g1, 1);
+    const unsigned right = __shfl_down_sync(0xffffffffu, g0, 1);
+    hgauss4(left, g0, g1, r.h[0], r.h[1]);
+    hgauss4(g0, g1, right, r.h[2], r.h[3]);
+    r.g[0] = g0;
+    r.g[1] = g1;
+  };
+
+  // Steps: at gy we have rows gy-4..gy; gauss row gc = gy-2.
+  auto step = [&](RowSlot& r4, RowSlot& r3, RowSlot& r2, RowSlot& r1, RowSlot& r0, int gy) {
+    // r4 = row gy-4 (oldest) ... r0 = row gy (just produced)
+    produce(r0, gy);
+    const int gc = gy - 2;
+    if (gc < y0 - 1 || gc > y0 + kBandRows) return;
+    unsigned gw[2];
+    if (gc < 2 || gc >= H - 2) {
+      gw[0] = r2.g[0];
+      gw[1] = r2.g[1];
+    } else {
+#pragma unroll
+      for (int w = 0; w < 2; ++w) {
+        const unsigned v0 = vgauss(r4.h[2 * w], r3.h[2 * w], r2.h[2 * w], r1.h[2 * w], r0.h[2 * w]);
+        const unsigned v1 =
+            vgauss(r4.h[2 * w + 1], r3.h[2 * w + 1], r2.h[2 * w + 1], r1.h[2 * w + 1], r0.h[2 * w + 1]);
+        const unsigned gauss = prmt(v0, v1, 0x7531);
+        gw[w] = lop_sel(gm[w], r2.g[w], gauss);
+      }
+    }
+    uint2* ps = prev_s + (gc - (y0 - 1)) * 32 + lane;
+    if (MODE == 0) {
+      *ps = make_uint2(gw[0], gw[1]);
+      return;
+    }
+    const uint2 pv = *ps;
+    *ps = make_uint2(gw[0], gw[1]);
+    r2.t[0] = thres4(gw[0], pv.x, g);
+    r2.t[1] = thres4(gw[1], pv.y, g);
+    if (next_tok && out_lane && gc >= y0 && gc < y0 + kBandRows && gc < H) {
+      store_bytes8<FAST>(next_tok, gc, x, W, gw[0], gw[1]);
+      if (next_copy) store_bytes8<FAST>(next_copy, gc, x, W, gw[0], gw[1]);
+    }
+    // Median of row m = gc - 1 (rows m-1, m, m+1 = r3 slot of gc-2 ... ).
+    const int m = gc - 1;
+    if (m < y0 || m >= y0 + kBandRows || m >= H) return;
+    // r3 holds row gc-1 = m, r4 holds gc-2 = m-1, r2 holds gc = m+1.
+    const unsigned c0 = r3.t[0], c1 = r3.t[1];
+    const unsigned lnb = __shfl_up_sync(0xffffffffu, c1, 1);
+    const unsigned rnb = __shfl_down_sync(0xffffffffu, c0, 1);
+    unsigned o0, o1;
+    if (m == 0 || m == H - 1) {
+      o0 = c0;
+      o1 = c1;
+    } else {
+      const unsigned l0 = __funnelshift_l(lnb, c0, 8), r0w = __funnelshift_r(c0, c1, 8);
+      const unsigned l1 = __funnelshift_l(c0, c1, 8), r1w = __funnelshift_r(c1, rnb, 8);
+      o0 = lop_sel(mm[0], c0, maj5(c0, r4.t[0], r2.t[0], l0, r0w));
+      o1 = lop_sel(mm[1], c1, maj5(c1, r4.t[1], r2.t[1], l1, r1w));
+    }
+    if (out_lane) store_bytes8<FAST>(out, m, x, W, prmt(o0, 0, 0xBA98), prmt(o1, 0, 0xBA98));
+  };
+
+  int gy = gy_begin;
+  // Prime rows y0-3 .. y0-0 (4 rows) so each step sees a full window.
+  produce(s[0], gy);
+  produce(s[1], gy + 1);
+  produce(s[2], gy + 2);
+  produce(s[3], gy + 3);
+  gy += 4;
+  while (true) {
+    if (gy >= gy_end) break;
+    step(s[0], s[1], s[2], s[3], s[4], gy++);
+    if (gy >= gy_end) break;
+    step(s[1], s[2], s[3], s[4], s[0], gy++);
+    if (gy >= gy_end) break;
+    step(s[2], s[3], s[4], s[0], s[1], gy++);
+    if (gy >= gy_end) break;
+    step(s[3], s[4], s[0], s[1], s[2], gy++);
+    if (gy >= gy_end) break;
+    step(s[4], s[0], s[1], s[2], s[3], gy++);
+  }
+}
+
+template <int FMT, bool FAST>
+__global__ void __launch_bounds__(32 * kWarpsPerCta) motion_fused_kernel(MotionIO io, MotionGeom g,
+                                                                         unsigned* done_counter) {
+  __shared__ uint2 prev_all[kWarpsPerCta][(kBandRows + 2) * 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int band = blockIdx.y * kWarpsPerCta + warp;
+  const int y0 = band * kBandRows;
+  const int x = (int)blockIdx.x * kOutPxPerWarp - kPxPerLane + lane * kPxPerLane;
+  const int f_begin = blockIdx.z * g.chunk;
+  const int f_end = min(f_begin + g.chunk, g.frames);
+  const size_t in_frame = (size_t)g.W * g.H * FMT;
+  const size_t frame_px = (size_t)g.W * g.H;
+
+  const unsigned char* in = io.in;
+  unsigned char* out = io.out;
+  const unsigned char* prev_tok = io.prev;
+  unsigned char* next_tok = io.next;
+  unsigned char* next_copy = io.next_copy;
+  if (io.channel_mode) {
+    in = chan_read_region(io.in_ch);
+    out = chan_write_region(io.out_ch);
+    prev_tok = chan_read_region(io.delay_ch);
+    next_tok = chan_write_region(io.delay_ch);
+    next_copy = chan_write_wraps(io.delay_ch) ? io.delay_ch.storage : nullptr;
+  }
+
+  if (y0 < g.H && f_begin < f_end) {
+    uint2* prev_s = prev_all[warp];
+    unsigned gm[2], mm[2];
+    column_masks(x, g.W, gm, mm);
+    if (f_begin == 0) {
+      // Delay token: gauss of the previous firing's last frame.
+      for (int r = 0; r < kBandRows + 2; ++r) {
+        unsigned a0, a1;
+        load_bytes8<FAST>(prev_tok, y0 - 1 + r, x, g.W, g.H, a0, a1);
+        prev_s[r * 32 + lane] = make_uint2(a0, a1);
+      }
+    } else {
+      frame_pass<FMT, FAST, 0>(in + (size_t)(f_begin - 1) * in_frame, nullptr, nullptr, nullptr,
+                               prev_s, g, y0, x, lane, gm, mm);
+    }
+    for (int f = f_begin; f < f_end; ++f) {
+      const bool last = (f == g.frames - 1);
+      frame_pass<FMT, FAST, 1>(in + (size_t)f * in_frame, out + (size_t)f * frame_px,
+                               last ? next_tok : nullptr, last ? next_copy : nullptr, prev_s, g,
+                               y0, x, lane, gm, mm);
+    }
+  }
+
+  if (io.channel_mode) {
+    __shared__ bool last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      last = atomicAdd(done_counter, 1u) == gridDim.x * gridDim.y * gridDim.z - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+      __threadfence();
+      *done_counter = 0;
+      chan_commit_read(io.in_ch, io.in_ch.rate);
+      chan_commit_read(io.delay_ch, 1);
+      chan_commit_write(io.delay_ch, 1);
+      chan_commit_write(io.out_ch, io.out_ch.rate);
+    }
+  }
+}
+
+// Gauss of one frame given in the input format (sets a delay token from a
+// raw halo frame).
+template <int FMT>
+__global__ void gauss_frame_kernel(const unsigned char* __restrict__ in, unsigned char* __restrict__ out,
+                                   int W, int H) {
+  const int xx = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
+  if (xx >= W) return;
+  auto gray = [&](int yy, int xi) -> int {
+    if (FMT == DF_MOTION_RGB) {
+      const unsigned char* q = in + ((size_t)yy * W + xi) * 3;
+      return (int)((77u * q[0] + 150u * q[1] + 29u * q[2] + 128u) >> 8);
+    }
+    return in[(size_t)yy * W + xi];
+  };
+  const size_t idx = (size_t)y * W + xx;
+  if (y < 2 || y >= H - 2 || xx < 2 || xx >= W - 2) {
+    out[idx] = (unsigned char)gray(y, xx);
+    return;
+  }
+  const int k[5] = {1, 4, 6, 4, 1};
+  int acc = 0;
+  for (int dy = -2; dy <= 2; ++dy)
+    for (int dx = -2; dx <= 2; ++dx) acc += k[dy + 2] * k[dx + 2] * gray(y + dy, xx + dx);
+  out[idx] = (unsigned char)((acc + 128) >> 8);
+}
+
+__global__ void thres_kernel(const unsigned char* prev, const unsigned char* cur, unsigned char* out,
+                             size_t n, int thr) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    out[i] = abs((int)cur[i] - (int)prev[i]) > thr ? 255 : 0;
+}
+
+__global__ void median_kernel(const unsigned char* in, unsigned char* out, int W, int H) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
+  if (x >= W) return;
+  const size_t i = (size_t)y * W + x;
+  if (y == 0 || y == H - 1 || x == 0 || x == W - 1) {
+    out[i] = in[i];
+    return;
+  }
+  unsigned char v[5] = {in[i], in[i - W], in[i + W], in[i - 1], in[i + 1]};
+  for (int a = 1; a < 5; ++a)
+    for (int b = a; b > 0 && v[b - 1] > v[b]; --b) {
+      unsigned char t = v[b];
+      v[b] = v[b - 1];
+      v[b - 1] = t;
+    }
+  out[i] = v[2];
+}
+
+__global__ void rgb_gray_kernel(const unsigned char* rgb, unsigned char* gray, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    gray[i] = (unsigned char)((77u * rgb[3 * i] + 150u * rgb[3 * i + 1] + 29u * rgb[3 * i + 2] + 128u) >> 8);
+}
+
+}  // namespace
+}  // namespace df
+
+using namespace df;
+
+struct df_motion {
+  int device = 0;
+  int W = 0, H = 0, fmt = 1;
+  uint8_t thr = 32;
+  unsigned char* tok[2] = {nullptr, nullptr};  // raw-mode delay token ping-pong
+  int cur = 0;
+  unsigned* scratch = nullptr;  // done counter
+  int resident_ctas = 0;        // per SM, for the temporal chunking
+  int sms = 148;
+};
+
+namespace {
+
+MotionGeom make_geom(const df_motion* m, int frames) {
+  MotionGeom g;
+  g.W = m->W;
+  g.H = m->H;
+  g.frames = frames;
+  const unsigned thr = m->thr;
+  if (thr <= 127) {
+    g.thr_k = (127u - thr) * 0x01010101u;
+    g.thr_sel = 0xFFFFFFFFu;
+  } else {
+    g.thr_k = (255u - thr) * 0x01010101u;
+    g.thr_sel = 0u;
+  }
+  // Temporal chunking: as many frame ranges as fit one wave of CTAs.
+  const int tiles = (m->W + kOutPxPerWarp - 1) / kOutPxPerWarp;
+  const int bands = (m->H + kBandRows - 1) / kBandRows;
+  const int ctas_per_chunk = tiles * ((bands + kWarpsPerCta - 1) / kWarpsPerCta);
+  const int wave = std::max(1, m->resident_ctas * m->sms);
+  int chunks = std::max(1, wave / std::max(1, ctas_per_chunk));
+  chunks = std::min(chunks, std::max(1, frames));
+  g.chunk = (frames + chunks - 1) / chunks;
+  return g;
+}
+
+template <int FMT, bool FAST>
+int launch_fused(df_motion* m, const MotionIO& io, int frames, cudaStream_t s) {
+  MotionGeom g = make_geom(m, frames);
+  const int tiles = (m->W + kOutPxPerWarp - 1) / kOutPxPerWarp;
+  const int bands = (m->H + kBandRows - 1) / kBandRows;
+  dim3 grid(tiles, (bands + kWarpsPerCta - 1) / kWarpsPerCta, (frames + g.chunk - 1) / g.chunk);
+  motion_fused_kernel<FMT, FAST><<<grid, 32 * kWarpsPerCta, 0, s>>>(io, g, m->scratch);
+  return after_launch("motion_fused_kernel");
+}
+
+int launch_motion(df_motion* m, const MotionIO& io, int frames, cudaStream_t s) {
+  if (frames <= 0) return DF_OK;
+  const bool fast = (m->W % 8 == 0);
+  if (m->fmt == DF_MOTION_RGB)
+    return fast ? launch_fused<DF_MOTION_RGB, true>(m, io, frames, s)
+                : launch_fused<DF_MOTION_RGB, false>(m, io, frames, s);
+  return fast ? launch_fused<DF_MOTION_GRAY, true>(m, io, frames, s)
+              : launch_fused<DF_MOTION_GRAY, false>(m, io, frames, s);
+}
+
+}  // namespace
+
+extern "C" {
+
+int df_motion_create(int device, unsigned width, unsigned height, int fmt, uint8_t thr,
+                     df_motion** out) {
+  DF_REQUIRE(out, DF_EINVAL, "df_motion_create: null out pointer");
+  *out = nullptr;
+  // proj/src/motion.cpp:108-110
+  DF_REQUIRE(width >= 5 && height >= 5, DF_EINVAL, "motion: frame must be at least 5x5");
+  DF_REQUIRE(fmt == DF_MOTION_GRAY || fmt == DF_MOTION_RGB, DF_EINVAL, "motion: input format must be GRAY or RGB");
+  DF_REQUIRE(width <= (1u << 20) && height <= (1u << 20), DF_EINVAL, "motion: frame too large");
+  DF_CHECK_CUDA(cudaSetDevice(device));
+  auto* m = new df_motion();
+  m->device = device;
+  m->W = (int)width;
+  m->H = (int)height;
+  m->fmt = fmt;
+  m->thr = thr;
+  const size_t px = (size_t)width * height;
+  cudaError_t e = cudaMalloc(&m->tok[0], px);
+  if (e == cudaSuccess) e = cudaMalloc(&m->tok[1], px);
+  if (e == cudaSuccess) e = cudaMalloc(&m->scratch, 64);
+  if (e == cudaSuccess) e = cudaMemset(m->tok[0], 0, px);  // black initial token
+  if (e == cudaSuccess) e = cudaMemset(m->scratch, 0, 64);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&m->sms, cudaDevAttrMultiProcessorCount, device);
+  if (e == cudaSuccess) {
+    const bool fast = width % 8 == 0;
+    const void* fn = fmt == DF_MOTION_RGB
+                         ? (fast ? (const void*)motion_fused_kernel<DF_MOTION_RGB, true>
+                                 : (const void*)motion_fused_kernel<DF_MOTION_RGB, false>)
+                         : (fast ? (const void*)motion_fused_kernel<DF_MOTION_GRAY, true>
+                                 : (const void*)motion_fused_kernel<DF_MOTION_GRAY, false>);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m->resident_ctas, fn, 32 * kWarpsPerCta, 0);
+  }
+  if (e != cudaSuccess) {
+    int rc = cuda_status(e, "df_motion_create");
+    cudaFree(m->tok[0]);
+    cudaFree(m->tok[1]);
+    cudaFree(m->scratch);
+    delete m;
+    return rc;
+  }
+  *out = m;
+  return DF_OK;
+}
+
+int df_motion_destroy(df_motion* m) {
+  if (!m) return DF_OK;
+  cudaSetDevice(m->device);
+  cudaFree(m->tok[0]);
+  cudaFree(m->tok[1]);
+  cudaFree(m->scratch);
+  delete m;
+  return DF_OK;
+}
+
+int df_motion_set_prev_frame(df_motion* m, const void* frame_dev, void* stream) {
+  DF_REQUIRE(m, DF_EINVAL, "df_motion_set_prev_frame: null actor");
+  DF_CHECK_CUDA(cudaSetDevice(m->device));
+  cudaStream_t s = as_stream(stream);
+  if (!frame_dev) {
+    DF_CHECK_CUDA(cudaMemsetAsync(m->tok[m->cur], 0, (size_t)m->W * m->H, s));
+    return DF_OK;
+  }
+  dim3 grid((m->W + 127) / 128, m->H);
+  if (m->fmt == DF_MOTION_RGB)
+    gauss_frame_kernel<DF_MOTION_RGB><<<grid, 128, 0, s>>>((const unsigned char*)frame_dev, m->tok[m->cur], m->W, m->H);
+  else
+    gauss_frame_kernel<DF_MOTION_GRAY><<<grid, 128, 0, s>>>((const unsigned char*)frame_dev, m->tok[m->cur], m->W, m->H);
+  return after_launch("gauss_frame_kernel");
+}
+
+int df_motion_fire(df_motion* m, const void* in_dev, uint8_t* out_dev, uint32_t frames, void* stream) {
+  DF_REQUIRE(m, DF_EINVAL, "df_motion_fire: null actor");
+  if (frames == 0) return DF_OK;
+  DF_REQUIRE(in_dev && out_dev, DF_EINVAL, "df_motion_fire: null buffer");
+  DF_REQUIRE(frames <= (1u << 30), DF_EINVAL, "df_motion_fire: too many frames");
+  DF_CHECK_CUDA(cudaSetDevice(m->device));
+  MotionIO io{};
+  io.in = (const unsigned char*)in_dev;
+  io.out = out_dev;
+  io.prev = m->tok[m->cur];
+  io.next = m->tok[m->cur ^ 1];
+  io.next_copy = nullptr;
+  io.channel_mode = 0;
+  DF_TRY(launch_motion(m, io, (int)frames, as_stream(stream)));
+  m->cur ^= 1;
+  return DF_OK;
+}
+
+int df_motion_fire_channels(df_motion* m, df_channel* in, df_channel* delay, df_channel* out,
+                            void* stream) {
+  DF_REQUIRE(m && in && delay && out, DF_EINVAL, "df_motion_fire_channels: null argument");
+  const size_t px = (size_t)m->W * m->H;
+  DF_REQUIRE(in->token_size == px * (size_t)m->fmt, DF_ELOGIC, "motion: input token must be one frame");
+  DF_REQUIRE(out->token_size == px && out->rate == in->rate, DF_ELOGIC,
+             "motion: output token must be one W*H mask at the input's rate");
+  DF_REQUIRE(delay->token_size == px && delay->rate == 1 && delay->has_delay, DF_ELOGIC,
+             "motion: delay channel must be a rate-1 self-loop with a delay token of W*H bytes");
+  DF_REQUIRE(in->reader != Endpoint::host && out->writer != Endpoint::host &&
+                 delay->reader != Endpoint::host && delay->writer != Endpoint::host,
+             DF_ELOGIC, "motion: channel endpoint is host-driven");
+  in->reader = out->writer = delay->reader = delay->writer = Endpoint::device;
+  DF_CHECK_CUDA(cudaSetDevice(m->device));
+  MotionIO io{};
+  io.channel_mode = 1;
+  io.in_ch = in->dev();
+  io.out_ch = out->dev();
+  io.delay_ch = delay->dev();
+  return launch_motion(m, io, (int)in->rate, as_stream(stream));
+}
+
+int df_motion_run_host(df_motion* m, const void* in_host, uint8_t* out_host, uint64_t frames,
+                       uint32_t chunk_frames, void* stream) {
+  DF_REQUIRE(m && in_host && out_host, DF_EINVAL, "df_motion_run_host: null argument");
+  if (frames == 0) return DF_OK;
+  DF_CHECK_CUDA(cudaSetDevice(m->device));
+  const size_t in_frame = (size_t)m->W * m->H * m->fmt, out_frame = (size_t)m->W * m->H;
+  if (chunk_frames == 0) chunk_frames = (uint32_t)std::max<size_t>(1, (96ull << 20) / in_frame);
+  chunk_frames = (uint32_t)std::min<uint64_t>(chunk_frames, frames);
+  cudaStream_t cs = as_stream(stream);
+  unsigned char* bin[2] = {nullptr, nullptr};
+  unsigned char* bout[2] = {nullptr, nullptr};
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t in_ready[2], comp_done[2], out_free[2];
+  int rc = DF_OK;
+  auto ck = [&](cudaError_t e, const char* w) {
+    if (rc == DF_OK && e != cudaSuccess) rc = cuda_status(e, w);
+    return rc == DF_OK;
+  };
+  ck(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking), "stream");
+  ck(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking), "stream");
+  for (int i = 0; i < 2; ++i) {
+    ck(cudaMalloc(&bin[i], chunk_frames * in_frame), "cudaMalloc");
+    ck(cudaMalloc(&bout[i], chunk_frames * out_frame), "cudaMalloc");
+    ck(cudaEventCreateWithFlags(&in_ready[i], cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&comp_done[i], cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&out_free[i], cudaEventDisableTiming), "event");
+  }
+  const uint64_t nchunks = (frames + chunk_frames - 1) / chunk_frames;
+  for (uint64_t c = 0; c < nchunks && rc == DF_OK; ++c) {
+    const int i = (int)(c & 1);
+    const uint64_t f0 = c * chunk_frames;
+    const uint32_t nf = (uint32_t)std::min<uint64_t>(chunk_frames, frames - f0);
+    if (c >= 2) ck(cudaStreamWaitEvent(h2d, comp_done[i], 0), "wait");
+    ck(cudaMemcpyAsync(bin[i], (const unsigned char*)in_host + f0 * in_frame, nf * in_frame,
+                       cudaMemcpyHostToDevice, h2d), "h2d");
+    ck(cudaEventRecord(in_ready[i], h2d), "record");
+    ck(cudaStreamWaitEvent(cs, in_ready[i], 0), "wait");
+    if (c >= 2) ck(cudaStreamWaitEvent(cs, out_free[i], 0), "wait");
+    if (rc != DF_OK) break;
+    rc = df_motion_fire(m, bin[i], bout[i], nf, cs);
+    ck(cudaEventRecord(comp_done[i], cs), "record");
+    ck(cudaStreamWaitEvent(d2h, comp_done[i], 0), "wait");
+    ck(cudaMemcpyAsync(out_host + f0 * out_frame, bout[i], nf * out_frame, cudaMemcpyDeviceToHost, d2h), "d2h");
+    ck(cudaEventRecord(out_free[i], d2h), "record");
+  }
+  ck(cudaStreamSynchronize(d2h), "sync");
+  ck(cudaStreamSynchronize(cs), "sync");
+  for (int i = 0; i < 2; ++i) {
+    cudaFree(bin[i]);
+    cudaFree(bout[i]);
+    cudaEventDestroy(in_ready[i]);
+    cudaEventDestroy(comp_done[i]);
+    cudaEventDestroy(out_free[i]);
+  }
+  if (h2d) cudaStreamDestroy(h2d);
+  if (d2h) cudaStreamDestroy(d2h);
+  return rc;
+}
+
+int df_motion_gauss5x5(const uint8_t* in_dev, uint8_t* out_dev, unsigned w, unsigned h, void* stream) {
+  DF_REQUIRE(in_dev && out_dev, DF_EINVAL, "gauss5x5: null buffer");
+  DF_REQUIRE(w >= 5 && h >= 5, DF_EINVAL, "gauss5x5: frame smaller than the 5x5 kernel");
+  dim3 grid((w + 127) / 128, h);
+  gauss_frame_kernel<DF_MOTION_GRAY><<<grid, 128, 0, as_stream(stream)>>>(in_dev, out_dev, (int)w, (int)h);
+  return after_launch("gauss_frame_kernel");
+}
+
+int df_motion_thres_diff(const uint8_t* prev_dev, const uint8_t* cur_dev, uint8_t* out_dev, unsigned w,
+                         unsigned h, uint8_t thr, void* stream) {
+  DF_REQUIRE(prev_dev && cur_dev && out_dev, DF_EINVAL, "thres_diff: null buffer");
+  const size_t n = (size_t)w * h;
+  if (n == 0) return DF_OK;
+  thres_kernel<<<(unsigned)std::min<size_t>((n + 255) / 256, 4096), 256, 0, as_stream(stream)>>>(
+      prev_dev, cur_dev, out_dev, n, thr);
+  return after_launch("thres_kernel");
+}
+
+int df_motion_median5(const uint8_t* in_dev, uint8_t* out_dev, unsigned w, unsigned h, void* stream) {
+  DF_REQUIRE(in_dev && out_dev, DF_EINVAL, "median5: null buffer");
+  DF_REQUIRE(w >= 3 && h >= 3, DF_EINVAL, "median5: frame smaller than 3x3");
+  dim3 grid((w + 127) / 128, h);
+  median_kernel<<<grid, 128, 0, as_stream(stream)>>>(in_dev, out_dev, (int)w, (int)h);
+  return after_launch("median_kernel");
+}
+
+int df_motion_rgb_to_gray(const uint8_t* rgb_dev, uint8_t* gray_dev, size_t pixels, void* stream) {
+  DF_REQUIRE(rgb_dev && gray_dev, DF_EINVAL, "rgb_to_gray: null buffer");
+  if (pixels == 0) return DF_OK;
+  rgb_gray_kernel<<<(unsigned)std::min<size_t>((pixels + 255) / 256, 4096), 256, 0, as_stream(stream)>>>(
+      rgb_dev, gray_dev, pixels);
+  return after_launch("rgb_gray_kernel");
+}
+
+}  // extern "C"
