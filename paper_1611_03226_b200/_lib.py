@@ -11,7 +11,7 @@ import os
 import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdf_cuda.so")
+LIB_PATH = os.environ.get("DF_CUDA_LIB", os.path.join(HERE, "libdf_cuda.so"))
 HEADER_PATH = os.path.join(os.path.dirname(HERE), "include", "df_cuda.h")
 
 DF_OK, DF_EINVAL, DF_ELOGIC, DF_EABORTED, DF_ECUDA, DF_ECONTROL, DF_EOS = range(7)

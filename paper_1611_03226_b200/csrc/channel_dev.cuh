@@ -75,18 +75,22 @@ __device__ inline void chan_commit_write(const DevChan& c, unsigned n) {
   if (n == 0) return;
   DevChanState* st = c.st;
   if (st->closed) chan_set_error(st, 2 /*DF_ELOGIC: write after close*/);
-  if (st->available + n > chan_distinct_capacity(c.rate, c.has_delay))
+  // The producer and consumer endpoints commit concurrently (different
+  // streams); `available` is the one shared counter (the reference guards it
+  // with its mutex, channel.cpp:106), so it is updated atomically.  Phases
+  // and written/read each have a single writer.
+  const unsigned long long before = atomicAdd(&st->available, (unsigned long long)n);
+  if (before + n > chan_distinct_capacity(c.rate, c.has_delay))
     chan_set_error(st, 2 /*DF_ELOGIC: overflow -- schedule violated capacity*/);
   st->write_phase = (st->write_phase + 1) % chan_phases(c.has_delay);
-  st->available += n;
   st->written += n;
 }
 __device__ inline void chan_commit_read(const DevChan& c, unsigned n) {
   if (n == 0) return;
   DevChanState* st = c.st;
-  if (st->available < n) chan_set_error(st, 2 /*DF_ELOGIC: underflow*/);
+  const unsigned long long before = atomicAdd(&st->available, (unsigned long long)(-(long long)n));
+  if (before < n) chan_set_error(st, 2 /*DF_ELOGIC: underflow*/);
   st->read_phase = (st->read_phase + 1) % chan_phases(c.has_delay);
-  st->available -= n;
   st->read += n;
 }
 #endif

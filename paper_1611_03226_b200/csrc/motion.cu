@@ -209,7 +209,8 @@ template <bool FAST>
 __device__ __forceinline__ void store_bytes8(unsigned char* __restrict__ plane, int y, int x, int W,
                                              unsigned a0, unsigned a1) {
   if (FAST) {
-    *reinterpret_cast<uint2*>(plane + (size_t)y * W + x) = make_uint2(a0, a1);
+    // W % 8 == 0: an 8-px segment is entirely inside or entirely outside.
+    if (x >= 0 && x < W) *reinterpret_cast<uint2*>(plane + (size_t)y * W + x) = make_uint2(a0, a1);
   } else {
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
