@@ -16,12 +16,14 @@
 //   fir   acc += (tr*xr - ti*xi); acc += (tr*xi + ti*xr), k ascending
 //           from 0.0f (dpd.cpp:87-104)
 //   adder out = 0.0f; out += y_b for active b ascending (dpd.cpp:306-320)
-// Two provable shortcuts: the leading "0.0f +" of the FIR accumulator and
-// of the adder are dropped and a single "+ 0.0f" is applied to the final
-// sum.  x + (+0) == x for every x != -0, the reference sums can never be
-// -0 (they start at +0 and an exact-zero sum rounds to +0), and dropping a
-// leading +0 only changes the sign of intermediate zeros -- so the final
-// "+ 0.0f" restores bit-identical output.
+// Two provable rewrites keep that bit-identical while saving work:
+//   * the FIR drops its leading "0.0f +" (tap 0 initialises the
+//     accumulator), which can only change the sign of an exact zero;
+//   * the branch sum starts from -0.0f, the exact additive identity, and
+//     the output gets one final "+ 0.0f".
+// x + (+0) == x for every x != -0, and the reference's sums can never be
+// -0 (they start at +0; an exact-zero sum rounds to +0), so the final
+// "+ 0.0f" restores the reference's bits exactly.
 //
 // FIR history across blocks.  Branch b's history at block p is the last
 // T-1 poly outputs of b's *active* stream before p (frozen while gated
@@ -209,42 +211,50 @@ __global__ void __launch_bounds__(THREADS) dpd_main_kernel(DpdIO io, const float
     const int w = tid + m * THREADS;
     const long long s = (long long)t0 - H1 + w;
     float2 v = make_float2(0.f, 0.f);
-    if (w < n + H1 && s >= 0) v = x[blk + s];
+    if (w < n + H1 && s >= 0) v = __ldg(&x[blk + s]);
     xr[m] = v.x;
     xi[m] = v.y;
     mg[m] = __fsqrt_rn(__fadd_rn(__fmul_rn(v.x, v.x), __fmul_rn(v.y, v.y)));
     sc[m] = 1.0f;
   }
 
+  // Branch sum starts at -0.0f, the exact additive identity (-0 + x == x
+  // for every x, including +0): the first add reproduces y_b bit for bit,
+  // and the final "+ 0.0f" maps an all-zero -0 to the reference's +0.
   float outr[V], outi[V];
-  bool first_branch = true;
+#pragma unroll
+  for (int j = 0; j < V; ++j) outr[j] = outi[j] = -0.0f;
   int prev_b = 1;
   int buf = 0;
 #pragma unroll 1
   for (uint32_t bits = mask; bits; bits &= bits - 1) {
     const int b = __ffs(bits);  // ascending branch order
-    // scale_b = scale_{prev}*mag^(b-prev): the reference's repeated product.
+    // scale_b = scale_prev * mag^(b - prev): the reference's repeated
+    // product 1*mag*mag... (1*mag == mag exactly).
+    if (prev_b == 1 && b > 1) {
 #pragma unroll
-    for (int m = 0; m < C::M; ++m) {
-      for (int q = prev_b; q < b; ++q) sc[m] = (q == 1) ? mg[m] : __fmul_rn(sc[m], mg[m]);
+      for (int m = 0; m < C::M; ++m) sc[m] = mg[m];
+      prev_b = 2;
     }
-    prev_b = b;
+#pragma unroll 1
+    for (; prev_b < b; ++prev_b) {
+#pragma unroll
+      for (int m = 0; m < C::M; ++m) sc[m] = __fmul_rn(sc[m], mg[m]);
+    }
     float2* u = us[buf];
 #pragma unroll
     for (int m = 0; m < C::M; ++m) {
       const int w = tid + m * THREADS;
-      if (w < C::W) {
-        const long long s = (long long)t0 - H1 + w;
-        float2 v;
-        if (s < 0) {
-          v = hist[((size_t)p * kBranches + (b - 1)) * H1 + (size_t)(-s - 1)];
-        } else if (b == 1) {
-          v = make_float2(xr[m], xi[m]);
-        } else {
-          v = make_float2(__fmul_rn(xr[m], sc[m]), __fmul_rn(xi[m], sc[m]));
-        }
+      if (m < C::M - 1 || w < C::W) {
+        float2 v = make_float2(xr[m], xi[m]);
+        if (b > 1) v = make_float2(__fmul_rn(xr[m], sc[m]), __fmul_rn(xi[m], sc[m]));
         u[pad_index(w)] = v;
       }
+    }
+    if (tile == 0 && tid < H1) {
+      // History before the block start: the branch's frozen FIR state as
+      // resolved by the prep kernel (u[-(j+1)] at window index H1-1-j).
+      u[pad_index(H1 - 1 - tid)] = hist[((size_t)p * kBranches + (b - 1)) * H1 + tid];
     }
     __syncthreads();
 
@@ -252,7 +262,6 @@ __global__ void __launch_bounds__(THREADS) dpd_main_kernel(DpdIO io, const float
     const float2* tb = taps_s + (b - 1) * T;
     float ar[V], ai[V], wr[V], wi[V];
     const int o0 = tid * V;
-    // Window for tap k = 0: u[o0 + H1 + j].
 #pragma unroll
     for (int j = 0; j < V; ++j) {
       const float2 v = u[pad_index(o0 + H1 + j)];
@@ -262,7 +271,7 @@ __global__ void __launch_bounds__(THREADS) dpd_main_kernel(DpdIO io, const float
     {
       const float2 t = tb[0];
 #pragma unroll
-      for (int j = 0; j < V; ++j) {  // tap 0 without the leading 0.0f +
+      for (int j = 0; j < V; ++j) {  // tap 0 without the leading 0.0f + (see header)
         ar[j] = __fsub_rn(__fmul_rn(t.x, wr[j]), __fmul_rn(t.y, wi[j]));
         ai[j] = __fadd_rn(__fmul_rn(t.x, wi[j]), __fmul_rn(t.y, wr[j]));
       }
@@ -285,25 +294,12 @@ __global__ void __launch_bounds__(THREADS) dpd_main_kernel(DpdIO io, const float
         ai[j] = __fadd_rn(ai[j], __fadd_rn(__fmul_rn(t.x, wi[j]), __fmul_rn(t.y, wr[j])));
       }
     }
-    if (first_branch) {
 #pragma unroll
-      for (int j = 0; j < V; ++j) {
-        outr[j] = ar[j];
-        outi[j] = ai[j];
-      }
-      first_branch = false;
-    } else {
-#pragma unroll
-      for (int j = 0; j < V; ++j) {
-        outr[j] = __fadd_rn(outr[j], ar[j]);
-        outi[j] = __fadd_rn(outi[j], ai[j]);
-      }
+    for (int j = 0; j < V; ++j) {
+      outr[j] = __fadd_rn(outr[j], ar[j]);
+      outi[j] = __fadd_rn(outi[j], ai[j]);
     }
     buf ^= 1;
-  }
-  if (first_branch) {  // no active branch: the adder emits +0.0f
-#pragma unroll
-    for (int j = 0; j < V; ++j) outr[j] = outi[j] = 0.0f;
   }
 
   // Stage through smem for coalesced stores (reuse the idle buffer).

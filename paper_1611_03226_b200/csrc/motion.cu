@@ -39,8 +39,8 @@
 namespace df {
 namespace {
 
-constexpr int kBandRows = 32;             // R
-constexpr int kWarpsPerCta = 4;
+constexpr int kBandRows = 48;             // R
+constexpr int kWarpsPerCta = 1;  // y0 depends on blockIdx only: warp-uniform for the compiler
 constexpr int kPxPerLane = 8;
 constexpr int kOutPxPerWarp = 30 * kPxPerLane;  // 240
 
@@ -107,6 +107,12 @@ __device__ __forceinline__ unsigned rgb4_to_gray(unsigned w0, unsigned w1, unsig
   return prmt(lo, hi, 0x5410);
 }
 
+__device__ __forceinline__ unsigned pack16x2(unsigned lo, unsigned hi) {
+  unsigned d;  // hi * 65536 + lo on the FMA pipe (keeps the ALU pipe for LOP3/PRMT)
+  asm("mad.lo.u32 %0, %1, 65536, %2;" : "=r"(d) : "r"(hi), "r"(lo));
+  return d;
+}
+
 // Horizontal [1 4 6 4 1] over 4 px of word C with neighbours L (left word)
 // and R (right word): two 16x2 packed pair words.
 __device__ __forceinline__ void hgauss4(unsigned L, unsigned C, unsigned R, unsigned& p01,
@@ -115,8 +121,8 @@ __device__ __forceinline__ void hgauss4(unsigned L, unsigned C, unsigned R, unsi
   const unsigned h1 = dp4a(L, W8(0, 0, 0, 1), dp4a(C, W8(4, 6, 4, 1), 0u));
   const unsigned h2 = dp4a(C, W8(1, 4, 6, 4), dp4a(R, W8(1, 0, 0, 0), 0u));
   const unsigned h3 = dp4a(C, W8(0, 1, 4, 6), dp4a(R, W8(4, 1, 0, 0), 0u));
-  p01 = prmt(h0, h1, 0x5410);
-  p23 = prmt(h2, h3, 0x5410);
+  p01 = pack16x2(h0, h1);
+  p23 = pack16x2(h2, h3);
 }
 
 // Vertical [1 4 6 4 1] on 16x2 lanes with +128, returns packed sums.
@@ -146,38 +152,67 @@ __device__ __forceinline__ unsigned maj5(unsigned c, unsigned u, unsigned d, uns
 }
 
 // --- row I/O -----------------------------------------------------------
-// Loads the 8 gray px [x, x+8) of row y (zeros outside the frame).
+// One row slot of the 5-row rolling window.  It also carries the raw loads
+// of the row 5 below (software prefetch riding the window rotation: slot k
+// is refilled with row r+5 exactly when row r leaves the window).
+template <int FMT>
+struct RowSlot {
+  unsigned h[4];   // horizontal sums, 16x2 packed: px (0,1), (2,3), (4,5), (6,7)
+  unsigned g[2];   // gray words
+  unsigned t[2];   // threshold flags (bit 7 per byte) once computed
+  uint2 raw[FMT == DF_MOTION_RGB ? 3 : 1];  // prefetched input of row (this + 5)
+  int raw_y;       // row index of raw (uniform)
+};
+
+// Issues the loads of row y into r.raw (FAST: aligned vector loads; the
+// values are consumed five rows later).  Out-of-frame rows/lanes load a
+// clamped in-bounds address and are zeroed at conversion.
 template <int FMT, bool FAST>
-__device__ __forceinline__ void load_gray8(const unsigned char* __restrict__ frame, int y, int x,
-                                           int W, int H, unsigned& g0, unsigned& g1) {
-  g0 = g1 = 0;
-  if (y < 0 || y >= H || x >= W || x + kPxPerLane <= 0) return;
+__device__ __forceinline__ void fetch_row(RowSlot<FMT>& r, const unsigned char* __restrict__ frame, int y,
+                                          int xc, int W, int H) {
+  r.raw_y = y;
+  if (!FAST) return;
+  const int yc = min(max(y, 0), H - 1);
+  if (FMT == DF_MOTION_RGB) {
+    const uint2* p = reinterpret_cast<const uint2*>(frame + ((size_t)yc * W + xc) * 3);
+    r.raw[0] = __ldg(p);
+    r.raw[1] = __ldg(p + 1);
+    r.raw[2] = __ldg(p + 2);
+  } else {
+    r.raw[0] = __ldg(reinterpret_cast<const uint2*>(frame + (size_t)yc * W + xc));
+  }
+}
+
+template <int FMT, bool FAST>
+__device__ __forceinline__ void convert_row(const RowSlot<FMT>& r, const unsigned char* __restrict__ frame,
+                                            int x, bool lane_in, int W, int H, unsigned& g0, unsigned& g1) {
+  const int y = r.raw_y;
+  const bool ok = lane_in && y >= 0 && y < H;
   if (FAST) {
     if (FMT == DF_MOTION_RGB) {
-      const uint2* p = reinterpret_cast<const uint2*>(frame + ((size_t)y * W + x) * 3);
-      const uint2 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
-      g0 = rgb4_to_gray(a.x, a.y, b.x);
-      g1 = rgb4_to_gray(b.y, c.x, c.y);
+      g0 = rgb4_to_gray(r.raw[0].x, r.raw[0].y, r.raw[1].x);
+      g1 = rgb4_to_gray(r.raw[1].y, r.raw[2].x, r.raw[2].y);
     } else {
-      const uint2 a = __ldg(reinterpret_cast<const uint2*>(frame + (size_t)y * W + x));
-      g0 = a.x;
-      g1 = a.y;
+      g0 = r.raw[0].x;
+      g1 = r.raw[0].y;
     }
+    g0 = ok ? g0 : 0u;
+    g1 = ok ? g1 : 0u;
   } else {
     unsigned char px[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int xi = x + i;
-      if (xi >= 0 && xi < W) {
+      unsigned char v = 0;
+      if (y >= 0 && y < H && xi >= 0 && xi < W) {
         if (FMT == DF_MOTION_RGB) {
           const unsigned char* q = frame + ((size_t)y * W + xi) * 3;
-          px[i] = (unsigned char)((77u * q[0] + 150u * q[1] + 29u * q[2] + 128u) >> 8);
+          v = (unsigned char)((77u * q[0] + 150u * q[1] + 29u * q[2] + 128u) >> 8);
         } else {
-          px[i] = frame[(size_t)y * W + xi];
+          v = frame[(size_t)y * W + xi];
         }
-      } else {
-        px[i] = 0;
       }
+      px[i] = v;
     }
     g0 = W8(px[0], px[1], px[2], px[3]);
     g1 = W8(px[4], px[5], px[6], px[7]);
@@ -220,13 +255,6 @@ __device__ __forceinline__ void store_bytes8(unsigned char* __restrict__ plane, 
   }
 }
 
-// One row slot of the 5-row rolling window.
-struct RowSlot {
-  unsigned h[4];   // horizontal sums, 16x2 packed: px (0,1), (2,3), (4,5), (6,7)
-  unsigned g[2];   // gray words
-  unsigned t[2];   // threshold flags (bit 7 per byte) once computed
-};
-
 // Byte masks (0xFF per byte) of columns in the gauss border (x < 2 or
 // x >= W-2) and the median border (x == 0 or x == W-1).
 __device__ __forceinline__ void column_masks(int x, int W, unsigned gm[2], unsigned mm[2]) {
@@ -252,17 +280,18 @@ __device__ __forceinline__ void frame_pass(const unsigned char* __restrict__ fra
                                            unsigned char* __restrict__ next_tok,
                                            unsigned char* __restrict__ next_copy,
                                            uint2* __restrict__ prev_s, const MotionGeom& g, int y0,
-                                           int x, int lane, const unsigned gm[2],
+                                           int x, int xc, bool lane_in, int lane, const unsigned gm[2],
                                            const unsigned mm[2]) {
   const int W = g.W, H = g.H;
   const bool out_lane = lane >= 1 && lane <= 30;
-  RowSlot s[5];
-  // Row gy's slot is s[(gy - (y0 - 3)) % 5].  Rows y0-3 .. y0+R+2.
+  RowSlot<FMT> s[5];
+  // Rows y0-3 .. y0+R+2 (h rows needed for gauss rows y0-1 .. y0+R).
   const int gy_begin = y0 - 3, gy_end = min(y0 + kBandRows + 3, H + 3);
 
-  auto produce = [&](RowSlot& r, int gy) {
+  auto produce = [&](RowSlot<FMT>& r, int gy) {
     unsigned g0, g1;
-    load_gray8<FMT, FAST>(frame, gy, x, W, H, g0, g1);
+    convert_row<FMT, FAST>(r, frame, x, lane_in, W, H, g0, g1);
+    if (gy + 5 < gy_end) fetch_row<FMT, FAST>(r, frame, gy + 5, xc, W, H);
     const unsigned left = __shfl_up_sync(0xffffffffu, g1, 1);
     const unsigned right = __shfl_down_sync(0xffffffffu, g0, 1);
     hgauss4(left, g0, g1, r.h[0], r.h[1]);
@@ -271,9 +300,9 @@ __device__ __forceinline__ void frame_pass(const unsigned char* __restrict__ fra
     r.g[1] = g1;
   };
 
-  // Steps: at gy we have rows gy-4..gy; gauss row gc = gy-2.
-  auto step = [&](RowSlot& r4, RowSlot& r3, RowSlot& r2, RowSlot& r1, RowSlot& r0, int gy) {
-    // r4 = row gy-4 (oldest) ... r0 = row gy (just produced)
+  // Step at gy: window rows gy-4..gy (r4 oldest .. r0 newest); gauss row gy-2.
+  auto step = [&](RowSlot<FMT>& r4, RowSlot<FMT>& r3, RowSlot<FMT>& r2, RowSlot<FMT>& r1, RowSlot<FMT>& r0,
+                  int gy) {
     produce(r0, gy);
     const int gc = gy - 2;
     if (gc < y0 - 1 || gc > y0 + kBandRows) return;
@@ -304,10 +333,9 @@ __device__ __forceinline__ void frame_pass(const unsigned char* __restrict__ fra
       store_bytes8<FAST>(next_tok, gc, x, W, gw[0], gw[1]);
       if (next_copy) store_bytes8<FAST>(next_copy, gc, x, W, gw[0], gw[1]);
     }
-    // Median of row m = gc - 1 (rows m-1, m, m+1 = r3 slot of gc-2 ... ).
+    // Median of row m = gc - 1: rows m-1, m, m+1 are r4, r3, r2.
     const int m = gc - 1;
     if (m < y0 || m >= y0 + kBandRows || m >= H) return;
-    // r3 holds row gc-1 = m, r4 holds gc-2 = m-1, r2 holds gc = m+1.
     const unsigned c0 = r3.t[0], c1 = r3.t[1];
     const unsigned lnb = __shfl_up_sync(0xffffffffu, c1, 1);
     const unsigned rnb = __shfl_down_sync(0xffffffffu, c0, 1);
@@ -325,7 +353,8 @@ __device__ __forceinline__ void frame_pass(const unsigned char* __restrict__ fra
   };
 
   int gy = gy_begin;
-  // Prime rows y0-3 .. y0-0 (4 rows) so each step sees a full window.
+#pragma unroll
+  for (int k = 0; k < 5; ++k) fetch_row<FMT, FAST>(s[k], frame, gy + k, xc, W, H);
   produce(s[0], gy);
   produce(s[1], gy + 1);
   produce(s[2], gy + 2);
@@ -348,11 +377,13 @@ __device__ __forceinline__ void frame_pass(const unsigned char* __restrict__ fra
 template <int FMT, bool FAST>
 __global__ void __launch_bounds__(32 * kWarpsPerCta) motion_fused_kernel(MotionIO io, MotionGeom g,
                                                                          unsigned* done_counter) {
-  __shared__ uint2 prev_all[kWarpsPerCta][(kBandRows + 2) * 32];
+  extern __shared__ uint2 prev_all[];  // [kWarpsPerCta][(kBandRows + 2) * 32]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int band = blockIdx.y * kWarpsPerCta + warp;
   const int y0 = band * kBandRows;
   const int x = (int)blockIdx.x * kOutPxPerWarp - kPxPerLane + lane * kPxPerLane;
+  const bool lane_in = x >= 0 && x < g.W;  // FAST: 8-px segments never straddle W
+  const int xc = lane_in ? x : 0;
   const int f_begin = blockIdx.z * g.chunk;
   const int f_end = min(f_begin + g.chunk, g.frames);
   const size_t in_frame = (size_t)g.W * g.H * FMT;
@@ -372,25 +403,26 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) motion_fused_kernel(MotionI
   }
 
   if (y0 < g.H && f_begin < f_end) {
-    uint2* prev_s = prev_all[warp];
+    uint2* prev_s = prev_all + warp * (kBandRows + 2) * 32;
     unsigned gm[2], mm[2];
     column_masks(x, g.W, gm, mm);
     if (f_begin == 0) {
       // Delay token: gauss of the previous firing's last frame.
+#pragma unroll 10
       for (int r = 0; r < kBandRows + 2; ++r) {
         unsigned a0, a1;
         load_bytes8<FAST>(prev_tok, y0 - 1 + r, x, g.W, g.H, a0, a1);
         prev_s[r * 32 + lane] = make_uint2(a0, a1);
       }
     } else {
-      frame_pass<FMT, FAST, 0>(in + (size_t)(f_begin - 1) * in_frame, nullptr, nullptr, nullptr,
-                               prev_s, g, y0, x, lane, gm, mm);
+      frame_pass<FMT, FAST, 0>(in + (size_t)(f_begin - 1) * in_frame, nullptr, nullptr, nullptr, prev_s, g,
+                               y0, x, xc, lane_in, lane, gm, mm);
     }
     for (int f = f_begin; f < f_end; ++f) {
       const bool last = (f == g.frames - 1);
       frame_pass<FMT, FAST, 1>(in + (size_t)f * in_frame, out + (size_t)f * frame_px,
-                               last ? next_tok : nullptr, last ? next_copy : nullptr, prev_s, g,
-                               y0, x, lane, gm, mm);
+                               last ? next_tok : nullptr, last ? next_copy : nullptr, prev_s, g, y0, x, xc,
+                               lane_in, lane, gm, mm);
     }
   }
 
@@ -412,6 +444,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) motion_fused_kernel(MotionI
     }
   }
 }
+
+constexpr size_t kSmemBytes = sizeof(uint2) * kWarpsPerCta * (kBandRows + 2) * 32;
 
 // Gauss of one frame given in the input format (sets a delay token from a
 // raw halo frame).
@@ -516,7 +550,7 @@ int launch_fused(df_motion* m, const MotionIO& io, int frames, cudaStream_t s) {
   const int tiles = (m->W + kOutPxPerWarp - 1) / kOutPxPerWarp;
   const int bands = (m->H + kBandRows - 1) / kBandRows;
   dim3 grid(tiles, (bands + kWarpsPerCta - 1) / kWarpsPerCta, (frames + g.chunk - 1) / g.chunk);
-  motion_fused_kernel<FMT, FAST><<<grid, 32 * kWarpsPerCta, 0, s>>>(io, g, m->scratch);
+  motion_fused_kernel<FMT, FAST><<<grid, 32 * kWarpsPerCta, kSmemBytes, s>>>(io, g, m->scratch);
   return after_launch("motion_fused_kernel");
 }
 
@@ -563,7 +597,9 @@ int df_motion_create(int device, unsigned width, unsigned height, int fmt, uint8
                                  : (const void*)motion_fused_kernel<DF_MOTION_RGB, false>)
                          : (fast ? (const void*)motion_fused_kernel<DF_MOTION_GRAY, true>
                                  : (const void*)motion_fused_kernel<DF_MOTION_GRAY, false>);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m->resident_ctas, fn, 32 * kWarpsPerCta, 0);
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+    if (e == cudaSuccess)
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m->resident_ctas, fn, 32 * kWarpsPerCta, kSmemBytes);
   }
   if (e != cudaSuccess) {
     int rc = cuda_status(e, "df_motion_create");
