@@ -1,0 +1,52 @@
+// df/dpd.hpp -- the dynamic predistortion network as GPU actors.
+//
+// Reference: dynflow::dpd (/root/reference/proj/include/dynflow/dpd.hpp,
+// proj/src/dpd.cpp:151-356): source -> split -> 10 x (poly -> fir10) ->
+// adder -> sink plus a config actor driving 12 control ports, one token of
+// `period` samples per firing.  B200 form: source (H2D) -> config (device
+// control tokens) -> dpd (ONE dynamic GPU actor: split/branches/adder fused,
+// its control token consumed on the device per logical firing) -> sink
+// (D2H).  A launch covers `batch` logical firings (channels run at rate
+// `batch`, one block token and one control token per logical firing).
+#pragma once
+
+#include <complex>
+#include <cstdint>
+#include <span>
+#include <vector>
+
+#include "df/model.hpp"
+
+struct df_dpd;
+
+namespace df::dpd {
+
+inline constexpr unsigned kBranchCount = 10;
+
+// dpd.hpp:26-36
+struct ConfigToken {
+  std::uint16_t active_mask = 0;
+  unsigned active_count() const { return __builtin_popcount(active_mask); }
+  bool active(unsigned branch) const { return (active_mask >> (branch - 1)) & 1u; }
+  static ConfigToken first_n(unsigned k) { return {static_cast<std::uint16_t>((1u << k) - 1)}; }
+};
+
+// check_config (dpd.cpp:49-58) with the single-branch extension:
+// k in [min_active, 10], no branch beyond 10.
+void check_config(ConfigToken token, unsigned min_active = 1);
+
+struct Params {
+  std::uint32_t period = 65536;       // samples per token (one block)
+  std::uint64_t samples = 0;          // multiple of period * batch
+  std::uint32_t taps_per_branch = 10;  // 10 = reference; up to 32
+  std::vector<std::complex<float>> taps;  // 10 * taps_per_branch, branch-major
+  std::vector<ConfigToken> schedule;      // one entry per block, cycling
+  std::uint32_t batch = 1;                // logical firings per launch
+  std::span<const std::complex<float>> input;  // host, interleaved re/im
+  std::span<std::complex<float>> output;
+};
+
+NetworkGraph build_network(const Params& params);
+std::uint64_t source_firings(const Params& params);  // launches
+
+}  // namespace df::dpd

@@ -1,0 +1,151 @@
+// df/model.hpp -- actor/port/channel model of the B200 GPU-actor runtime.
+//
+// Same vocabulary and rules as the reference's dynflow model
+// (/root/reference/proj/include/dynflow/model.hpp:14-193): ChannelSpec,
+// PortSpec, ActorSpec, ActorBehavior, build_network, validate.  What
+// changes for GPU actors: channel storage lives in HBM (df_channel), a
+// firing ENQUEUES device work on the actor's stream, and a dynamic GPU
+// actor's control function runs on the device (it consumes its control
+// token from the device ring), so `ActorBehavior::control` is replaced by
+// `device_control = true`.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <functional>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+struct df_channel;
+
+namespace df {
+
+enum class PortDirection { input, output };
+enum class PortKind { regular, control };
+enum class ActorKind { static_rate, dynamic_rate };
+
+// model.hpp:21-25
+struct PortSpec {
+  PortDirection direction = PortDirection::input;
+  PortKind kind = PortKind::regular;
+  std::string channel_id;
+};
+
+// model.hpp:31-37 -- token_rate tokens per firing on both endpoints;
+// has_delay: one initial token (initial_token_value or zeros).
+struct ChannelSpec {
+  std::string id;
+  std::size_t token_size = 1;
+  std::uint32_t token_rate = 1;
+  bool has_delay = false;
+  std::vector<std::byte> initial_token_value;
+};
+
+// Per-firing view handed to a GPU actor's fire function: the device
+// channels bound to its ports (declaration order, regular ports only, the
+// control channel separately) and the CUDA stream to enqueue on.  Region
+// addresses and (for dynamic actors) token counts are resolved by the
+// device; the host never dereferences channel storage.
+class FiringContext {
+ public:
+  std::size_t input_count() const { return inputs_.size(); }
+  std::size_t output_count() const { return outputs_.size(); }
+  df_channel* input(std::size_t i) const { return inputs_.at(i); }
+  df_channel* output(std::size_t i) const { return outputs_.at(i); }
+  df_channel* control() const { return control_; }
+  void* stream() const { return stream_; }
+  int device() const { return device_; }
+  std::uint64_t firing_index() const { return firing_index_; }
+
+  // Assembled by the runtime.
+  void reset(std::uint64_t firing, void* stream, int device) {
+    firing_index_ = firing;
+    stream_ = stream;
+    device_ = device;
+  }
+  void bind(std::vector<df_channel*> in, std::vector<df_channel*> out, df_channel* ctrl) {
+    inputs_ = std::move(in);
+    outputs_ = std::move(out);
+    control_ = ctrl;
+  }
+
+ private:
+  std::vector<df_channel*> inputs_, outputs_;
+  df_channel* control_ = nullptr;
+  void* stream_ = nullptr;
+  int device_ = 0;
+  std::uint64_t firing_index_ = 0;
+};
+
+// model.hpp:103-108: mandatory fire; optional init / finish.  A dynamic
+// GPU actor sets device_control: its kernels consume one control token per
+// logical firing on the device (rates 0 or r decided there).
+struct ActorBehavior {
+  std::function<void(FiringContext&)> fire;
+  std::function<void()> init;
+  std::function<void()> finish;
+  bool device_control = false;
+};
+
+struct ActorSpec {
+  std::string id;
+  ActorKind kind = ActorKind::static_rate;
+  std::vector<PortSpec> ports;
+  ActorBehavior behavior;
+};
+
+struct ChannelEndpoints {
+  std::size_t producer_actor = npos, producer_port = npos;
+  std::size_t consumer_actor = npos, consumer_port = npos;
+  static constexpr std::size_t npos = static_cast<std::size_t>(-1);
+};
+
+class BuildError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+class ControlError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+
+struct Violation {
+  std::string subject;
+  std::string message;
+  bool operator==(const Violation&) const = default;
+};
+
+class NetworkGraph {
+ public:
+  const std::vector<ActorSpec>& actors() const { return actors_; }
+  const std::vector<ChannelSpec>& channels() const { return channels_; }
+  const std::vector<ChannelEndpoints>& endpoints() const { return endpoints_; }
+  std::size_t actor_index(const std::string& id) const;
+  std::size_t channel_index(const std::string& id) const;
+  std::vector<std::size_t> regular_ports(std::size_t actor) const;
+  std::optional<std::size_t> control_port(std::size_t actor) const;
+
+  friend NetworkGraph build_network(std::vector<ActorSpec> actors, std::vector<ChannelSpec> channels);
+
+ private:
+  std::vector<ActorSpec> actors_;
+  std::vector<ChannelSpec> channels_;
+  std::vector<ChannelEndpoints> endpoints_;
+};
+
+// Structural assembly, BuildError on defects (model.cpp:45-102 semantics).
+NetworkGraph build_network(std::vector<ActorSpec> actors, std::vector<ChannelSpec> channels);
+
+// Rule checks, ordered by channel id, actor id, then structure
+// (model.cpp:104-238): rates/sizes >= 1, initial tokens only with a delay,
+// control channels rate 1 without delay, one control port per dynamic
+// actor, no undelayed cycles.  A delayed self-loop is legal.
+std::vector<Violation> validate(const NetworkGraph& net);
+
+// Eq. 1 (channel.cpp:9-16).
+std::size_t capacity_tokens(const ChannelSpec& spec);
+std::size_t capacity_bytes(const ChannelSpec& spec);
+
+}  // namespace df

@@ -1,0 +1,33 @@
+// df/motion.hpp -- the motion-detection network as GPU actors.
+//
+// Reference: dynflow::motion (/root/reference/proj/src/motion.cpp:107-218):
+// source -> gauss -> (cur, prev with a one-frame delay token) -> thres ->
+// med -> sink.  B200 form: source (H2D) -> motion (ONE fused GPU actor:
+// gray/gauss/thres/median; the prev stream is a rate-1 self-loop delay
+// channel carrying gauss of the last frame, black initially) -> sink (D2H).
+#pragma once
+
+#include <cstdint>
+#include <span>
+
+#include "df/model.hpp"
+
+namespace df::motion {
+
+enum class Input { gray = 1, rgb = 3 };
+
+struct Params {
+  unsigned width = 320;
+  unsigned height = 240;
+  std::uint8_t threshold = 32;
+  std::uint32_t token_rate = 1;  // frames per firing
+  std::uint64_t frames = 0;      // multiple of token_rate
+  Input input_format = Input::gray;
+  std::span<const std::uint8_t> input;  // frames * width * height * format bytes (host)
+  std::span<std::uint8_t> output;       // frames * width * height bytes (host)
+};
+
+NetworkGraph build_network(const Params& params);
+std::uint64_t source_firings(const Params& params);
+
+}  // namespace df::motion

@@ -1,0 +1,45 @@
+/*
+ * df_host.h -- C ABI of libdf_host.so: the C++ GPU-actor runtime (include/df/)
+ * running the two reference networks end to end from HOST buffers.
+ *
+ * These are the drop-in calls for the reference's network runs
+ * (/root/reference/proj/src/bench.cpp:383-441 cmd_dpd and :328-381
+ * cmd_motion: build_network(params) + run(net, cfg) with host spans), as a
+ * cgo/ctypes/JNI binding would call them.  Status 0 = OK; on failure
+ * dfh_last_error() describes the exception (ValidationError,
+ * std::invalid_argument, ActorFault naming the actor, ...).
+ */
+#ifndef DF_HOST_H
+#define DF_HOST_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+const char* dfh_last_error(void);
+
+/* taps: 10 * taps_per_branch complex (re, im) floats, branch-major;
+ * schedule: one 10-bit mask per block (bit b-1 = branch b), cycling.
+ * samples % (period * batch) == 0.  sink_active_ms: device time of the
+ * sink actor from its first to its last firing (like active_seconds). */
+int dfh_dpd_run(int device, const float* in_host, float* out_host, uint64_t samples, uint32_t period,
+                uint32_t taps_per_branch, const float* taps, const uint16_t* schedule, size_t schedule_len,
+                uint32_t batch, double* sink_active_ms, uint64_t* dpd_firings);
+
+/* input_format: 1 gray, 3 RGB; frames % token_rate == 0. */
+int dfh_motion_run(int device, const uint8_t* in_host, uint8_t* out_host, uint64_t frames, unsigned width,
+                   unsigned height, int input_format, uint8_t threshold, uint32_t token_rate,
+                   double* sink_active_ms, uint64_t* delay_tokens_written);
+
+/* Host-side rule checks (no device): builds the named reference network
+ * shape and returns the number of validate() violations (0 = runnable);
+ * -1 with dfh_last_error() on a BuildError / invalid_argument. */
+int dfh_validate_demo(int which);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

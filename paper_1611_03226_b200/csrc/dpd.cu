@@ -40,6 +40,7 @@
 #include "channel_dev.cuh"
 #include "channel_host.hpp"
 #include "common.cuh"
+#include "staging.cuh"
 
 namespace df {
 namespace {
@@ -419,6 +420,7 @@ struct df_dpd {
   unsigned long long ctrl_cap = 0;
   uint16_t* sched_dev = nullptr;
   size_t sched_cap = 0;
+  df::Staging staging;  // df_dpd_run_host pipeline
 };
 
 namespace {
@@ -533,6 +535,7 @@ int df_dpd_destroy(df_dpd* d) {
   cudaFree(d->act);
   cudaFree(d->ctrl_buf);
   cudaFree(d->sched_dev);
+  d->staging.release();
   delete d;
   return DF_OK;
 }
@@ -647,78 +650,51 @@ int df_dpd_run_host(df_dpd* d, const float* in_host, float* out_host, uint64_t s
   if (samples == 0) return DF_OK;
   DF_CHECK_CUDA(cudaSetDevice(d->device));
   const uint64_t blocks = samples / d->period;
-  if (chunk_blocks == 0) chunk_blocks = std::max<uint64_t>(1, (64ull << 20) / (8ull * d->period));
+  if (chunk_blocks == 0) chunk_blocks = std::max<uint64_t>(1, (128ull << 20) / (8ull * d->period));
   chunk_blocks = std::min(chunk_blocks, blocks);
   const size_t chunk_bytes = chunk_blocks * d->period * 8ull;
   cudaStream_t cs = as_stream(stream);
-  // Two slots of (in, out) buffers; copies on dedicated streams.
-  float* bin[2] = {nullptr, nullptr};
-  float* bout[2] = {nullptr, nullptr};
-  uint32_t* ctrl = nullptr;
-  uint16_t* sd = nullptr;
-  cudaStream_t h2d = nullptr, d2h = nullptr;
-  cudaEvent_t in_ready[2], comp_done[2], out_free[2];
-  int rc = DF_OK;
-  auto ck = [&](cudaError_t e, const char* w) {
-    if (rc == DF_OK && e != cudaSuccess) rc = cuda_status(e, w);
-    return rc == DF_OK;
-  };
-  ck(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking), "stream");
-  ck(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking), "stream");
-  for (int i = 0; i < 2; ++i) {
-    ck(cudaMalloc(&bin[i], chunk_bytes), "cudaMalloc");
-    ck(cudaMalloc(&bout[i], chunk_bytes), "cudaMalloc");
-    ck(cudaEventCreateWithFlags(&in_ready[i], cudaEventDisableTiming), "event");
-    ck(cudaEventCreateWithFlags(&comp_done[i], cudaEventDisableTiming), "event");
-    ck(cudaEventCreateWithFlags(&out_free[i], cudaEventDisableTiming), "event");
+  DF_TRY(d->staging.ensure(chunk_bytes, chunk_bytes));
+  if (blocks > d->ctrl_cap) {
+    DF_CHECK_CUDA(cudaDeviceSynchronize());
+    cudaFree(d->ctrl_buf);
+    d->ctrl_buf = nullptr;
+    DF_CHECK_CUDA(cudaMalloc(&d->ctrl_buf, blocks * sizeof(uint32_t)));
+    d->ctrl_cap = blocks;
   }
-  ck(cudaMalloc(&ctrl, blocks * sizeof(uint32_t)), "cudaMalloc");
-  ck(cudaMalloc(&sd, schedule_len * sizeof(uint16_t)), "cudaMalloc");
-  ck(cudaMemcpyAsync(sd, schedule_host, schedule_len * sizeof(uint16_t), cudaMemcpyHostToDevice, cs), "copy");
-  if (rc == DF_OK) {
-    // Config actor: one control token per block, on device.
-    dpd_config_kernel<<<(unsigned)std::min<uint64_t>((blocks + 255) / 256, 1184), 256, 0, cs>>>(
-        sd, (unsigned)schedule_len, 0, blocks, ctrl);
-    rc = after_launch("dpd_config_kernel");
+  if (schedule_len > d->sched_cap) {
+    DF_CHECK_CUDA(cudaDeviceSynchronize());
+    cudaFree(d->sched_dev);
+    d->sched_dev = nullptr;
+    DF_CHECK_CUDA(cudaMalloc(&d->sched_dev, schedule_len * sizeof(uint16_t)));
+    d->sched_cap = schedule_len;
   }
-  // Slot reuse ordering: in slot i is free once compute of chunk c-2 is
-  // done (comp_done); out slot i is free once its D2H is done (out_free).
+  uint32_t* ctrl = static_cast<uint32_t*>(d->ctrl_buf);
+  DF_CHECK_CUDA(cudaMemcpyAsync(d->sched_dev, schedule_host, schedule_len * sizeof(uint16_t),
+                                cudaMemcpyHostToDevice, cs));
+  // Config actor: one control token per block, on device.
+  dpd_config_kernel<<<(unsigned)std::min<uint64_t>((blocks + 255) / 256, 1184), 256, 0, cs>>>(
+      d->sched_dev, (unsigned)schedule_len, 0, blocks, ctrl);
+  DF_TRY(after_launch("dpd_config_kernel"));
   const uint64_t nchunks = (blocks + chunk_blocks - 1) / chunk_blocks;
-  for (uint64_t c = 0; c < nchunks && rc == DF_OK; ++c) {
-    const int i = (int)(c & 1);
-    const uint64_t b0 = c * chunk_blocks;
-    const uint64_t nb = std::min(chunk_blocks, blocks - b0);
-    const size_t bytes = nb * d->period * 8ull;
-    if (c >= 2) ck(cudaStreamWaitEvent(h2d, comp_done[i], 0), "wait");
-    ck(cudaMemcpyAsync(bin[i], in_host + 2 * b0 * d->period, bytes, cudaMemcpyHostToDevice, h2d), "h2d");
-    ck(cudaEventRecord(in_ready[i], h2d), "record");
-    ck(cudaStreamWaitEvent(cs, in_ready[i], 0), "wait");
-    if (c >= 2) ck(cudaStreamWaitEvent(cs, out_free[i], 0), "wait");
-    if (rc != DF_OK) break;
-    DpdIO io{};
-    io.ctrl = ctrl + b0;
-    io.in = reinterpret_cast<const float2*>(bin[i]);
-    io.out = reinterpret_cast<float2*>(bout[i]);
-    rc = launch_dpd(d, io, nb, cs);
-    ck(cudaEventRecord(comp_done[i], cs), "record");
-    ck(cudaStreamWaitEvent(d2h, comp_done[i], 0), "wait");
-    ck(cudaMemcpyAsync(out_host + 2 * b0 * d->period, bout[i], bytes, cudaMemcpyDeviceToHost, d2h), "d2h");
-    ck(cudaEventRecord(out_free[i], d2h), "record");
-  }
-  ck(cudaStreamSynchronize(d2h), "sync");
-  ck(cudaStreamSynchronize(cs), "sync");
-  for (int i = 0; i < 2; ++i) {
-    cudaFree(bin[i]);
-    cudaFree(bout[i]);
-    cudaEventDestroy(in_ready[i]);
-    cudaEventDestroy(comp_done[i]);
-    cudaEventDestroy(out_free[i]);
-  }
-  cudaFree(ctrl);
-  cudaFree(sd);
-  if (h2d) cudaStreamDestroy(h2d);
-  if (d2h) cudaStreamDestroy(d2h);
-  return rc;
+  auto nb = [&](uint64_t c) { return std::min(chunk_blocks, blocks - c * chunk_blocks); };
+  return d->staging.pipeline(
+      cs, nchunks,
+      [&](uint64_t c, const void*& p, size_t& b) {
+        p = in_host + 2 * c * chunk_blocks * d->period;
+        b = nb(c) * d->period * 8ull;
+      },
+      [&](uint64_t c, void*& p, size_t& b) {
+        p = out_host + 2 * c * chunk_blocks * d->period;
+        b = nb(c) * d->period * 8ull;
+      },
+      [&](uint64_t c, unsigned char* din, unsigned char* dout) {
+        DpdIO io{};
+        io.ctrl = ctrl + c * chunk_blocks;
+        io.in = reinterpret_cast<const float2*>(din);
+        io.out = reinterpret_cast<float2*>(dout);
+        return launch_dpd(d, io, nb(c), cs);
+      });
 }
 
 }  // extern "C"

@@ -35,6 +35,7 @@
 #include "channel_dev.cuh"
 #include "channel_host.hpp"
 #include "common.cuh"
+#include "staging.cuh"
 
 namespace df {
 namespace {
@@ -60,6 +61,10 @@ struct MotionGeom {
   int chunk;         // frames per temporal chunk
   unsigned thr_k;    // SWAR constant
   unsigned thr_sel;  // 0xFFFFFFFF if thr <= 127 else 0
+  // IDP.4A weight words, passed as kernel parameters so every dp4a takes
+  // its weights straight from the constant bank (no per-step UMOVs).
+  unsigned wg[6];    // gray
+  unsigned wh[8];    // horizontal gauss
 };
 
 __device__ __forceinline__ unsigned dp4a(unsigned a, unsigned b, unsigned c) {
@@ -97,11 +102,13 @@ constexpr unsigned W8(unsigned a, unsigned b, unsigned c, unsigned d) {
 }
 
 // 4 gray bytes from 12 interleaved RGB bytes (w0,w1,w2 little endian).
-__device__ __forceinline__ unsigned rgb4_to_gray(unsigned w0, unsigned w1, unsigned w2) {
-  const unsigned r0 = dp4a(w0, W8(77, 150, 29, 0), 128u);
-  const unsigned r1 = dp4a(w1, W8(150, 29, 0, 0), dp4a(w0, W8(0, 0, 0, 77), 128u));
-  const unsigned r2 = dp4a(w2, W8(29, 0, 0, 0), dp4a(w1, W8(0, 0, 77, 150), 128u));
-  const unsigned r3 = dp4a(w2, W8(0, 77, 150, 29), 128u);
+// wg = {W8(77,150,29,0), W8(150,29,0,0), W8(0,0,0,77), W8(29,0,0,0),
+//       W8(0,0,77,150), W8(0,77,150,29)}.
+__device__ __forceinline__ unsigned rgb4_to_gray(unsigned w0, unsigned w1, unsigned w2, const unsigned* wg) {
+  const unsigned r0 = dp4a(w0, wg[0], 128u);
+  const unsigned r1 = dp4a(w1, wg[1], dp4a(w0, wg[2], 128u));
+  const unsigned r2 = dp4a(w2, wg[3], dp4a(w1, wg[4], 128u));
+  const unsigned r3 = dp4a(w2, wg[5], 128u);
   const unsigned lo = prmt(r0, r1, 0x0051);  // bytes [r0.b1, r1.b1]
   const unsigned hi = prmt(r2, r3, 0x0051);
   return prmt(lo, hi, 0x5410);
@@ -114,23 +121,27 @@ __device__ __forceinline__ unsigned pack16x2(unsigned lo, unsigned hi) {
 }
 
 // Horizontal [1 4 6 4 1] over 4 px of word C with neighbours L (left word)
-// and R (right word): two 16x2 packed pair words.
+// and R (right word): two 16x2 packed pair words.  Each sum carries a +8
+// bias (dp4a accumulator): the vertical weights sum to 16, so the bias
+// adds exactly the +128 of (acc + 128) >> 8 (motion.cpp:45).
+// wh = {W8(0,0,1,4), W8(6,4,1,0), W8(0,0,0,1), W8(4,6,4,1), W8(1,4,6,4),
+//       W8(1,0,0,0), W8(0,1,4,6), W8(4,1,0,0)}.
 __device__ __forceinline__ void hgauss4(unsigned L, unsigned C, unsigned R, unsigned& p01,
-                                        unsigned& p23) {
-  const unsigned h0 = dp4a(L, W8(0, 0, 1, 4), dp4a(C, W8(6, 4, 1, 0), 0u));
-  const unsigned h1 = dp4a(L, W8(0, 0, 0, 1), dp4a(C, W8(4, 6, 4, 1), 0u));
-  const unsigned h2 = dp4a(C, W8(1, 4, 6, 4), dp4a(R, W8(1, 0, 0, 0), 0u));
-  const unsigned h3 = dp4a(C, W8(0, 1, 4, 6), dp4a(R, W8(4, 1, 0, 0), 0u));
+                                        unsigned& p23, const unsigned* wh) {
+  const unsigned h0 = dp4a(L, wh[0], dp4a(C, wh[1], 8u));
+  const unsigned h1 = dp4a(L, wh[2], dp4a(C, wh[3], 8u));
+  const unsigned h2 = dp4a(C, wh[4], dp4a(R, wh[5], 8u));
+  const unsigned h3 = dp4a(C, wh[6], dp4a(R, wh[7], 8u));
   p01 = pack16x2(h0, h1);
   p23 = pack16x2(h2, h3);
 }
 
-// Vertical [1 4 6 4 1] on 16x2 lanes with +128, returns packed sums.
+// Vertical [1 4 6 4 1] on 16x2 lanes (the +128 rides in the h bias);
+// max 16 * (4080 + 8) = 65408 < 2^16, so lanes never carry.
 __device__ __forceinline__ unsigned vgauss(unsigned a, unsigned b, unsigned c, unsigned d,
                                           unsigned e) {
-  const unsigned A = a + e + 0x00800080u;
   const unsigned B = b + d;
-  return c * 6u + (B * 4u + A);
+  return c * 6u + (B * 4u + (a + e));
 }
 
 // |cur - prev| > thr per byte -> flag in bit 7 (other bits don't-care).
@@ -165,33 +176,35 @@ struct RowSlot {
 };
 
 // Issues the loads of row y into r.raw (FAST: aligned vector loads; the
-// values are consumed five rows later).  Out-of-frame rows/lanes load a
-// clamped in-bounds address and are zeroed at conversion.
+// values are consumed five rows later).  The row index is clamped into the
+// frame (warp-uniform), out-of-frame lanes read a clamped column; both are
+// zeroed at conversion.
 template <int FMT, bool FAST>
-__device__ __forceinline__ void fetch_row(RowSlot<FMT>& r, const unsigned char* __restrict__ frame, int y,
-                                          int xc, int W, int H) {
+__device__ __forceinline__ void fetch_row(RowSlot<FMT>& r, const unsigned char* __restrict__ frame,
+                                          unsigned lane_off, int y, int H, unsigned row_bytes) {
   r.raw_y = y;
   if (!FAST) return;
-  const int yc = min(max(y, 0), H - 1);
+  const unsigned yc = (unsigned)min(max(y, 0), H - 1);
+  const uint2* p = reinterpret_cast<const uint2*>(frame + (yc * row_bytes + lane_off));
   if (FMT == DF_MOTION_RGB) {
-    const uint2* p = reinterpret_cast<const uint2*>(frame + ((size_t)yc * W + xc) * 3);
     r.raw[0] = __ldg(p);
     r.raw[1] = __ldg(p + 1);
     r.raw[2] = __ldg(p + 2);
   } else {
-    r.raw[0] = __ldg(reinterpret_cast<const uint2*>(frame + (size_t)yc * W + xc));
+    r.raw[0] = __ldg(p);
   }
 }
 
 template <int FMT, bool FAST>
 __device__ __forceinline__ void convert_row(const RowSlot<FMT>& r, const unsigned char* __restrict__ frame,
-                                            int x, bool lane_in, int W, int H, unsigned& g0, unsigned& g1) {
+                                            int x, bool lane_in, int W, int H, unsigned& g0, unsigned& g1,
+                                            const unsigned* wg) {
   const int y = r.raw_y;
-  const bool ok = lane_in && y >= 0 && y < H;
   if (FAST) {
+    const bool ok = lane_in && (unsigned)y < (unsigned)H;
     if (FMT == DF_MOTION_RGB) {
-      g0 = rgb4_to_gray(r.raw[0].x, r.raw[0].y, r.raw[1].x);
-      g1 = rgb4_to_gray(r.raw[1].y, r.raw[2].x, r.raw[2].y);
+      g0 = rgb4_to_gray(r.raw[0].x, r.raw[0].y, r.raw[1].x, wg);
+      g1 = rgb4_to_gray(r.raw[1].y, r.raw[2].x, r.raw[2].y, wg);
     } else {
       g0 = r.raw[0].x;
       g1 = r.raw[0].y;
@@ -225,7 +238,7 @@ __device__ __forceinline__ void load_bytes8(const unsigned char* __restrict__ pl
   a0 = a1 = 0;
   if (y < 0 || y >= H || x >= W || x + kPxPerLane <= 0) return;
   if (FAST) {
-    const uint2 a = *reinterpret_cast<const uint2*>(plane + (size_t)y * W + x);
+    const uint2 a = *reinterpret_cast<const uint2*>(plane + ((unsigned)y * (unsigned)W + (unsigned)x));
     a0 = a.x;
     a1 = a.y;
   } else {
@@ -245,7 +258,8 @@ __device__ __forceinline__ void store_bytes8(unsigned char* __restrict__ plane, 
                                              unsigned a0, unsigned a1) {
   if (FAST) {
     // W % 8 == 0: an 8-px segment is entirely inside or entirely outside.
-    if (x >= 0 && x < W) *reinterpret_cast<uint2*>(plane + (size_t)y * W + x) = make_uint2(a0, a1);
+    if (x >= 0 && x < W)
+      *reinterpret_cast<uint2*>(plane + ((unsigned)y * (unsigned)W + (unsigned)x)) = make_uint2(a0, a1);
   } else {
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -274,6 +288,7 @@ __device__ __forceinline__ void column_masks(int x, int W, unsigned gm[2], unsig
 
 // Processes one frame for this warp's (tile, band).  MODE 0: gauss only,
 // into the prev buffer (warm-up of a frame range).  MODE 1: full chain.
+// MODE 2: full chain + writes the next delay token (last frame of a firing).
 template <int FMT, bool FAST, int MODE>
 __device__ __forceinline__ void frame_pass(const unsigned char* __restrict__ frame,
                                            unsigned char* __restrict__ out,
@@ -284,30 +299,27 @@ __device__ __forceinline__ void frame_pass(const unsigned char* __restrict__ fra
                                            const unsigned mm[2]) {
   const int W = g.W, H = g.H;
   const bool out_lane = lane >= 1 && lane <= 30;
+  const unsigned row_bytes = (unsigned)W * FMT;  // a frame is < 4 GiB (checked at create)
+  const unsigned lane_off = (unsigned)xc * FMT;
   RowSlot<FMT> s[5];
-  // Rows y0-3 .. y0+R+2 (h rows needed for gauss rows y0-1 .. y0+R).
-  const int gy_begin = y0 - 3, gy_end = min(y0 + kBandRows + 3, H + 3);
 
   auto produce = [&](RowSlot<FMT>& r, int gy) {
     unsigned g0, g1;
-    convert_row<FMT, FAST>(r, frame, x, lane_in, W, H, g0, g1);
-    if (gy + 5 < gy_end) fetch_row<FMT, FAST>(r, frame, gy + 5, xc, W, H);
+    convert_row<FMT, FAST>(r, frame, x, lane_in, W, H, g0, g1, g.wg);
+    fetch_row<FMT, FAST>(r, frame, lane_off, gy + 5, H, row_bytes);  // rows past the band are harmless
     const unsigned left = __shfl_up_sync(0xffffffffu, g1, 1);
     const unsigned right = __shfl_down_sync(0xffffffffu, g0, 1);
-    hgauss4(left, g0, g1, r.h[0], r.h[1]);
-    hgauss4(g0, g1, right, r.h[2], r.h[3]);
+    hgauss4(left, g0, g1, r.h[0], r.h[1], g.wh);
+    hgauss4(g0, g1, right, r.h[2], r.h[3], g.wh);
     r.g[0] = g0;
     r.g[1] = g1;
   };
 
-  // Step at gy: window rows gy-4..gy (r4 oldest .. r0 newest); gauss row gy-2.
-  auto step = [&](RowSlot<FMT>& r4, RowSlot<FMT>& r3, RowSlot<FMT>& r2, RowSlot<FMT>& r1, RowSlot<FMT>& r0,
-                  int gy) {
-    produce(r0, gy);
-    const int gc = gy - 2;
-    if (gc < y0 - 1 || gc > y0 + kBandRows) return;
+  // gauss + thres of row gc = gy - 2 (window r4..r0 = rows gy-4..gy).
+  auto gauss_thres = [&](RowSlot<FMT>& r4, RowSlot<FMT>& r3, RowSlot<FMT>& r2, RowSlot<FMT>& r1,
+                         RowSlot<FMT>& r0, int gc) {
     unsigned gw[2];
-    if (gc < 2 || gc >= H - 2) {
+    if ((unsigned)(gc - 2) >= (unsigned)(H - 4)) {  // gc < 2 || gc >= H-2: gray copied
       gw[0] = r2.g[0];
       gw[1] = r2.g[1];
     } else {
@@ -316,8 +328,7 @@ __device__ __forceinline__ void frame_pass(const unsigned char* __restrict__ fra
         const unsigned v0 = vgauss(r4.h[2 * w], r3.h[2 * w], r2.h[2 * w], r1.h[2 * w], r0.h[2 * w]);
         const unsigned v1 =
             vgauss(r4.h[2 * w + 1], r3.h[2 * w + 1], r2.h[2 * w + 1], r1.h[2 * w + 1], r0.h[2 * w + 1]);
-        const unsigned gauss = prmt(v0, v1, 0x7531);
-        gw[w] = lop_sel(gm[w], r2.g[w], gauss);
+        gw[w] = lop_sel(gm[w], r2.g[w], prmt(v0, v1, 0x7531));
       }
     }
     uint2* ps = prev_s + (gc - (y0 - 1)) * 32 + lane;
@@ -329,18 +340,19 @@ __device__ __forceinline__ void frame_pass(const unsigned char* __restrict__ fra
     *ps = make_uint2(gw[0], gw[1]);
     r2.t[0] = thres4(gw[0], pv.x, g);
     r2.t[1] = thres4(gw[1], pv.y, g);
-    if (next_tok && out_lane && gc >= y0 && gc < y0 + kBandRows && gc < H) {
+    if (MODE == 2 && out_lane && gc >= y0 && gc < y0 + kBandRows && gc < H) {
       store_bytes8<FAST>(next_tok, gc, x, W, gw[0], gw[1]);
       if (next_copy) store_bytes8<FAST>(next_copy, gc, x, W, gw[0], gw[1]);
     }
-    // Median of row m = gc - 1: rows m-1, m, m+1 are r4, r3, r2.
-    const int m = gc - 1;
-    if (m < y0 || m >= y0 + kBandRows || m >= H) return;
+  };
+
+  // Median of row m (rows m-1, m, m+1 = r4, r3, r2); always inside the band.
+  auto median = [&](RowSlot<FMT>& r4, RowSlot<FMT>& r3, RowSlot<FMT>& r2, int m) {
     const unsigned c0 = r3.t[0], c1 = r3.t[1];
     const unsigned lnb = __shfl_up_sync(0xffffffffu, c1, 1);
     const unsigned rnb = __shfl_down_sync(0xffffffffu, c0, 1);
     unsigned o0, o1;
-    if (m == 0 || m == H - 1) {
+    if ((unsigned)(m - 1) >= (unsigned)(H - 2)) {  // m == 0 || m == H-1: copied
       o0 = c0;
       o1 = c1;
     } else {
@@ -352,25 +364,35 @@ __device__ __forceinline__ void frame_pass(const unsigned char* __restrict__ fra
     if (out_lane) store_bytes8<FAST>(out, m, x, W, prmt(o0, 0, 0xBA98), prmt(o1, 0, 0xBA98));
   };
 
-  int gy = gy_begin;
+  // One step per gauss row gc (y0-1 .. gc_end): window rows gc-2..gc+2 are
+  // already produced; the step computes gauss/thres(gc) and median(gc-1)
+  // from them and, independently (ILP), produces row gc+3 into the slot of
+  // row gc-2 once that row has been consumed.
+  const int gc_end = min(y0 + kBandRows, H);  // last gauss row needed
+  auto step = [&](RowSlot<FMT>& r4, RowSlot<FMT>& r3, RowSlot<FMT>& r2, RowSlot<FMT>& r1, RowSlot<FMT>& r0,
+                  int gc) {
+    // r4..r0 = rows gc-2 .. gc+2
+    gauss_thres(r4, r3, r2, r1, r0, gc);
+    if (MODE != 0 && gc > y0) median(r4, r3, r2, gc - 1);  // rows gc-2, gc-1, gc
+    if (gc < gc_end) produce(r4, gc + 3);
+  };
+
+  int gc = y0 - 1;
 #pragma unroll
-  for (int k = 0; k < 5; ++k) fetch_row<FMT, FAST>(s[k], frame, gy + k, xc, W, H);
-  produce(s[0], gy);
-  produce(s[1], gy + 1);
-  produce(s[2], gy + 2);
-  produce(s[3], gy + 3);
-  gy += 4;
+  for (int k = 0; k < 5; ++k) fetch_row<FMT, FAST>(s[k], frame, lane_off, y0 - 3 + k, H, row_bytes);
+#pragma unroll
+  for (int k = 0; k < 5; ++k) produce(s[k], y0 - 3 + k);
   while (true) {
-    if (gy >= gy_end) break;
-    step(s[0], s[1], s[2], s[3], s[4], gy++);
-    if (gy >= gy_end) break;
-    step(s[1], s[2], s[3], s[4], s[0], gy++);
-    if (gy >= gy_end) break;
-    step(s[2], s[3], s[4], s[0], s[1], gy++);
-    if (gy >= gy_end) break;
-    step(s[3], s[4], s[0], s[1], s[2], gy++);
-    if (gy >= gy_end) break;
-    step(s[4], s[0], s[1], s[2], s[3], gy++);
+    if (gc > gc_end) break;
+    step(s[0], s[1], s[2], s[3], s[4], gc++);
+    if (gc > gc_end) break;
+    step(s[1], s[2], s[3], s[4], s[0], gc++);
+    if (gc > gc_end) break;
+    step(s[2], s[3], s[4], s[0], s[1], gc++);
+    if (gc > gc_end) break;
+    step(s[3], s[4], s[0], s[1], s[2], gc++);
+    if (gc > gc_end) break;
+    step(s[4], s[0], s[1], s[2], s[3], gc++);
   }
 }
 
@@ -418,12 +440,13 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) motion_fused_kernel(MotionI
       frame_pass<FMT, FAST, 0>(in + (size_t)(f_begin - 1) * in_frame, nullptr, nullptr, nullptr, prev_s, g,
                                y0, x, xc, lane_in, lane, gm, mm);
     }
-    for (int f = f_begin; f < f_end; ++f) {
-      const bool last = (f == g.frames - 1);
-      frame_pass<FMT, FAST, 1>(in + (size_t)f * in_frame, out + (size_t)f * frame_px,
-                               last ? next_tok : nullptr, last ? next_copy : nullptr, prev_s, g, y0, x, xc,
-                               lane_in, lane, gm, mm);
-    }
+    const int f_last = (f_end == g.frames) ? f_end - 1 : f_end;  // frame that emits the delay token
+    for (int f = f_begin; f < f_last; ++f)
+      frame_pass<FMT, FAST, 1>(in + (size_t)f * in_frame, out + (size_t)f * frame_px, nullptr, nullptr, prev_s,
+                               g, y0, x, xc, lane_in, lane, gm, mm);
+    if (f_last < f_end)
+      frame_pass<FMT, FAST, 2>(in + (size_t)f_last * in_frame, out + (size_t)f_last * frame_px, next_tok,
+                               next_copy, prev_s, g, y0, x, xc, lane_in, lane, gm, mm);
   }
 
   if (io.channel_mode) {
@@ -516,6 +539,7 @@ struct df_motion {
   unsigned* scratch = nullptr;  // done counter
   int resident_ctas = 0;        // per SM, for the temporal chunking
   int sms = 148;
+  df::Staging staging;          // df_motion_run_host pipeline
 };
 
 namespace {
@@ -533,6 +557,12 @@ MotionGeom make_geom(const df_motion* m, int frames) {
     g.thr_k = (255u - thr) * 0x01010101u;
     g.thr_sel = 0u;
   }
+  const unsigned wg[6] = {W8(77, 150, 29, 0), W8(150, 29, 0, 0), W8(0, 0, 0, 77),
+                          W8(29, 0, 0, 0),   W8(0, 0, 77, 150), W8(0, 77, 150, 29)};
+  const unsigned wh[8] = {W8(0, 0, 1, 4), W8(6, 4, 1, 0), W8(0, 0, 0, 1), W8(4, 6, 4, 1),
+                          W8(1, 4, 6, 4), W8(1, 0, 0, 0), W8(0, 1, 4, 6), W8(4, 1, 0, 0)};
+  for (int i = 0; i < 6; ++i) g.wg[i] = wg[i];
+  for (int i = 0; i < 8; ++i) g.wh[i] = wh[i];
   // Temporal chunking: as many frame ranges as fit one wave of CTAs.
   const int tiles = (m->W + kOutPxPerWarp - 1) / kOutPxPerWarp;
   const int bands = (m->H + kBandRows - 1) / kBandRows;
@@ -575,7 +605,8 @@ int df_motion_create(int device, unsigned width, unsigned height, int fmt, uint8
   // proj/src/motion.cpp:108-110
   DF_REQUIRE(width >= 5 && height >= 5, DF_EINVAL, "motion: frame must be at least 5x5");
   DF_REQUIRE(fmt == DF_MOTION_GRAY || fmt == DF_MOTION_RGB, DF_EINVAL, "motion: input format must be GRAY or RGB");
-  DF_REQUIRE(width <= (1u << 20) && height <= (1u << 20), DF_EINVAL, "motion: frame too large");
+  DF_REQUIRE(width <= (1u << 20) && height <= (1u << 20) && (uint64_t)width * height * 3 < (1ull << 32),
+             DF_EINVAL, "motion: frame too large");
   DF_CHECK_CUDA(cudaSetDevice(device));
   auto* m = new df_motion();
   m->device = device;
@@ -616,6 +647,7 @@ int df_motion_create(int device, unsigned width, unsigned height, int fmt, uint8
 int df_motion_destroy(df_motion* m) {
   if (!m) return DF_OK;
   cudaSetDevice(m->device);
+  m->staging.release();
   cudaFree(m->tok[0]);
   cudaFree(m->tok[1]);
   cudaFree(m->scratch);
@@ -685,57 +717,23 @@ int df_motion_run_host(df_motion* m, const void* in_host, uint8_t* out_host, uin
   if (frames == 0) return DF_OK;
   DF_CHECK_CUDA(cudaSetDevice(m->device));
   const size_t in_frame = (size_t)m->W * m->H * m->fmt, out_frame = (size_t)m->W * m->H;
-  if (chunk_frames == 0) chunk_frames = (uint32_t)std::max<size_t>(1, (96ull << 20) / in_frame);
+  if (chunk_frames == 0) chunk_frames = (uint32_t)std::max<size_t>(1, (256ull << 20) / in_frame);
   chunk_frames = (uint32_t)std::min<uint64_t>(chunk_frames, frames);
   cudaStream_t cs = as_stream(stream);
-  unsigned char* bin[2] = {nullptr, nullptr};
-  unsigned char* bout[2] = {nullptr, nullptr};
-  cudaStream_t h2d = nullptr, d2h = nullptr;
-  cudaEvent_t in_ready[2], comp_done[2], out_free[2];
-  int rc = DF_OK;
-  auto ck = [&](cudaError_t e, const char* w) {
-    if (rc == DF_OK && e != cudaSuccess) rc = cuda_status(e, w);
-    return rc == DF_OK;
-  };
-  ck(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking), "stream");
-  ck(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking), "stream");
-  for (int i = 0; i < 2; ++i) {
-    ck(cudaMalloc(&bin[i], chunk_frames * in_frame), "cudaMalloc");
-    ck(cudaMalloc(&bout[i], chunk_frames * out_frame), "cudaMalloc");
-    ck(cudaEventCreateWithFlags(&in_ready[i], cudaEventDisableTiming), "event");
-    ck(cudaEventCreateWithFlags(&comp_done[i], cudaEventDisableTiming), "event");
-    ck(cudaEventCreateWithFlags(&out_free[i], cudaEventDisableTiming), "event");
-  }
+  DF_TRY(m->staging.ensure(chunk_frames * in_frame, chunk_frames * out_frame));
   const uint64_t nchunks = (frames + chunk_frames - 1) / chunk_frames;
-  for (uint64_t c = 0; c < nchunks && rc == DF_OK; ++c) {
-    const int i = (int)(c & 1);
-    const uint64_t f0 = c * chunk_frames;
-    const uint32_t nf = (uint32_t)std::min<uint64_t>(chunk_frames, frames - f0);
-    if (c >= 2) ck(cudaStreamWaitEvent(h2d, comp_done[i], 0), "wait");
-    ck(cudaMemcpyAsync(bin[i], (const unsigned char*)in_host + f0 * in_frame, nf * in_frame,
-                       cudaMemcpyHostToDevice, h2d), "h2d");
-    ck(cudaEventRecord(in_ready[i], h2d), "record");
-    ck(cudaStreamWaitEvent(cs, in_ready[i], 0), "wait");
-    if (c >= 2) ck(cudaStreamWaitEvent(cs, out_free[i], 0), "wait");
-    if (rc != DF_OK) break;
-    rc = df_motion_fire(m, bin[i], bout[i], nf, cs);
-    ck(cudaEventRecord(comp_done[i], cs), "record");
-    ck(cudaStreamWaitEvent(d2h, comp_done[i], 0), "wait");
-    ck(cudaMemcpyAsync(out_host + f0 * out_frame, bout[i], nf * out_frame, cudaMemcpyDeviceToHost, d2h), "d2h");
-    ck(cudaEventRecord(out_free[i], d2h), "record");
-  }
-  ck(cudaStreamSynchronize(d2h), "sync");
-  ck(cudaStreamSynchronize(cs), "sync");
-  for (int i = 0; i < 2; ++i) {
-    cudaFree(bin[i]);
-    cudaFree(bout[i]);
-    cudaEventDestroy(in_ready[i]);
-    cudaEventDestroy(comp_done[i]);
-    cudaEventDestroy(out_free[i]);
-  }
-  if (h2d) cudaStreamDestroy(h2d);
-  if (d2h) cudaStreamDestroy(d2h);
-  return rc;
+  auto nf = [&](uint64_t c) { return (uint32_t)std::min<uint64_t>(chunk_frames, frames - c * chunk_frames); };
+  return m->staging.pipeline(
+      cs, nchunks,
+      [&](uint64_t c, const void*& p, size_t& b) {
+        p = (const unsigned char*)in_host + c * chunk_frames * in_frame;
+        b = nf(c) * in_frame;
+      },
+      [&](uint64_t c, void*& p, size_t& b) {
+        p = out_host + c * chunk_frames * out_frame;
+        b = nf(c) * out_frame;
+      },
+      [&](uint64_t c, unsigned char* din, unsigned char* dout) { return df_motion_fire(m, din, dout, nf(c), cs); });
 }
 
 int df_motion_gauss5x5(const uint8_t* in_dev, uint8_t* out_dev, unsigned w, unsigned h, void* stream) {

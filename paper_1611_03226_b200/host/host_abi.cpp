@@ -1,0 +1,155 @@
+// host_abi.cpp -- extern "C" entry points of libdf_host.so (df_host.h).
+#include <complex>
+#include <cstring>
+#include <string>
+
+#include "df/dpd.hpp"
+#include "df/motion.hpp"
+#include "df/runtime.hpp"
+#include "df_host.h"
+
+namespace {
+thread_local std::string g_err;
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const df::ActorFault& e) {
+    g_err = std::string("ActorFault: ") + e.what();
+    return 3;
+  } catch (const df::ValidationError& e) {
+    g_err = std::string("ValidationError: ") + e.what();
+    return 4;
+  } catch (const df::BuildError& e) {
+    g_err = std::string("BuildError: ") + e.what();
+    return 7;
+  } catch (const df::ControlError& e) {
+    g_err = std::string("ControlError: ") + e.what();
+    return 5;
+  } catch (const std::invalid_argument& e) {
+    g_err = std::string("invalid_argument: ") + e.what();
+    return 1;
+  } catch (const std::logic_error& e) {
+    g_err = std::string("logic_error: ") + e.what();
+    return 2;
+  } catch (const std::exception& e) {
+    g_err = std::string("error: ") + e.what();
+    return 6;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+const char* dfh_last_error(void) { return g_err.c_str(); }
+
+int dfh_dpd_run(int device, const float* in_host, float* out_host, uint64_t samples, uint32_t period,
+                uint32_t T, const float* taps, const uint16_t* schedule, size_t schedule_len, uint32_t batch,
+                double* sink_active_ms, uint64_t* dpd_firings) {
+  return guarded([&] {
+    df::dpd::Params p;
+    p.period = period;
+    p.samples = samples;
+    p.taps_per_branch = T;
+    p.taps.resize(std::size_t(10) * T);
+    for (std::size_t i = 0; i < p.taps.size(); ++i) p.taps[i] = {taps[2 * i], taps[2 * i + 1]};
+    for (size_t i = 0; i < schedule_len; ++i) p.schedule.push_back({schedule[i]});
+    p.batch = batch;
+    p.input = {reinterpret_cast<const std::complex<float>*>(in_host), samples};
+    p.output = {reinterpret_cast<std::complex<float>*>(out_host), samples};
+    df::NetworkGraph net = df::dpd::build_network(p);
+    df::ExecutionConfig cfg;
+    cfg.device = device;
+    cfg.source_firing_limit = df::dpd::source_firings(p);
+    df::RunStats st = df::run(net, cfg);
+    if (sink_active_ms) *sink_active_ms = st.actor("sink").active_ms;
+    if (dpd_firings) *dpd_firings = st.firings("dpd");
+  });
+}
+
+int dfh_motion_run(int device, const uint8_t* in_host, uint8_t* out_host, uint64_t frames, unsigned width,
+                   unsigned height, int fmt, uint8_t threshold, uint32_t rate, double* sink_active_ms,
+                   uint64_t* delay_tokens_written) {
+  return guarded([&] {
+    df::motion::Params p;
+    p.width = width;
+    p.height = height;
+    p.threshold = threshold;
+    p.token_rate = rate;
+    p.frames = frames;
+    p.input_format = fmt == 3 ? df::motion::Input::rgb : df::motion::Input::gray;
+    const std::size_t px = std::size_t(width) * height;
+    p.input = {in_host, frames * px * static_cast<unsigned>(fmt == 3 ? 3 : 1)};
+    p.output = {out_host, frames * px};
+    df::NetworkGraph net = df::motion::build_network(p);
+    df::ExecutionConfig cfg;
+    cfg.device = device;
+    cfg.source_firing_limit = df::motion::source_firings(p);
+    df::RunStats st = df::run(net, cfg);
+    if (sink_active_ms) *sink_active_ms = st.actor("sink").active_ms;
+    if (delay_tokens_written)
+      for (const auto& c : st.channels)
+        if (c.id == "motion_delay") *delay_tokens_written = c.tokens_written;
+  });
+}
+
+int dfh_validate_demo(int which) {
+  int n = -1;
+  int rc = guarded([&] {
+    using namespace df;
+    auto noop = [](FiringContext&) {};
+    std::vector<ActorSpec> actors;
+    std::vector<ChannelSpec> chans;
+    if (which == 0) {  // the GPU DPD network shape: valid
+      static std::vector<std::complex<float>> io(64), taps(100);
+      dpd::Params p;
+      p.period = 16;
+      p.samples = 64;
+      p.batch = 2;
+      p.taps = taps;
+      p.schedule = {dpd::ConfigToken::first_n(1), dpd::ConfigToken::first_n(10)};
+      p.input = io;
+      p.output = io;
+      n = (int)validate(dpd::build_network(p)).size();
+      return;
+    }
+    if (which == 1) {  // undelayed cycle a -> b -> a, static actor with control port
+      chans = {{"ab", 4, 1, false, {}}, {"ba", 4, 1, false, {}}, {"c", 4, 1, false, {}}};
+      ActorBehavior b;
+      b.fire = noop;
+      actors.push_back({"a", ActorKind::static_rate,
+                        {{PortDirection::output, PortKind::regular, "ab"},
+                         {PortDirection::input, PortKind::regular, "ba"},
+                         {PortDirection::output, PortKind::regular, "c"}},
+                        b});
+      actors.push_back({"b", ActorKind::static_rate,
+                        {{PortDirection::input, PortKind::regular, "ab"},
+                         {PortDirection::output, PortKind::regular, "ba"},
+                         {PortDirection::input, PortKind::control, "c"}},
+                        b});
+      n = (int)validate(build_network(actors, chans)).size();
+      return;
+    }
+    if (which == 2) {  // delayed self-loop: valid
+      chans = {{"loop", 8, 1, true, {}}};
+      ActorBehavior b;
+      b.fire = noop;
+      actors.push_back({"m", ActorKind::static_rate,
+                        {{PortDirection::input, PortKind::regular, "loop"},
+                         {PortDirection::output, PortKind::regular, "loop"}},
+                        b});
+      n = (int)validate(build_network(actors, chans)).size();
+      return;
+    }
+    // which == 3: BuildError (unknown channel)
+    ActorBehavior b;
+    b.fire = noop;
+    actors.push_back({"x", ActorKind::static_rate, {{PortDirection::output, PortKind::regular, "nope"}}, b});
+    build_network(actors, chans);
+  });
+  return rc == 0 ? n : -1;
+}
+
+}  // extern "C"

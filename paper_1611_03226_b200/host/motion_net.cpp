@@ -1,0 +1,80 @@
+// motion_net.cpp -- the motion-detection network as GPU actors
+// (reference network: /root/reference/proj/src/motion.cpp:107-218).
+#include <memory>
+#include <stdexcept>
+
+#include "df/motion.hpp"
+#include "df/runtime.hpp"
+#include "df_cuda.h"
+
+namespace df::motion {
+
+std::uint64_t source_firings(const Params& p) { return p.frames / p.token_rate; }
+
+NetworkGraph build_network(const Params& p) {
+  // motion.cpp:108-120
+  if (p.width < 5 || p.height < 5) throw std::invalid_argument("motion: frame must be at least 5x5");
+  if (p.token_rate < 1) throw std::invalid_argument("motion: token rate must be >= 1");
+  if (p.frames % p.token_rate != 0)
+    throw std::invalid_argument("motion: frame count must be a multiple of the token rate");
+  const std::size_t px = std::size_t(p.width) * p.height;
+  const std::size_t in_frame = px * static_cast<unsigned>(p.input_format);
+  if (p.input.size() != p.frames * in_frame || p.output.size() != p.frames * px)
+    throw std::invalid_argument("motion: input/output buffers must hold exactly `frames` frames");
+
+  const std::uint32_t r = p.token_rate;
+  auto input = p.input;
+  auto output = p.output;
+  std::vector<ChannelSpec> channels = {
+      {"src_motion", in_frame, r, false, {}},
+      // motion.cpp:131 "gauss_thres_prev": one-frame delay, black initial
+      // token -- here a self-loop carrying gauss(last frame) across firings
+      {"motion_delay", px, 1, true, {}},
+      {"motion_sink", px, r, false, {}},
+  };
+  std::vector<ActorSpec> actors;
+
+  ActorBehavior source;  // motion.cpp:137-142
+  source.fire = [input, in_frame, r](FiringContext& ctx) {
+    df_region reg;
+    check(df_channel_write_start(ctx.output(0), r, &reg));
+    check(df_memcpy_h2d(reg.dptr, input.data() + ctx.firing_index() * r * in_frame, in_frame * r, ctx.stream()));
+    check(df_channel_write_end(ctx.output(0), &reg, ctx.stream()));
+  };
+  actors.push_back({"source", ActorKind::static_rate, {{PortDirection::output, PortKind::regular, "src_motion"}},
+                    std::move(source)});
+
+  struct MotionState {
+    df_motion* h = nullptr;
+    ~MotionState() { df_motion_destroy(h); }
+  };
+  auto st = std::make_shared<MotionState>();
+  const unsigned w = p.width, h = p.height, thr = p.threshold;
+  const int fmt = static_cast<int>(p.input_format);
+  ActorBehavior fused;  // gauss + thres + med actors (motion.cpp:144-176), fused
+  fused.fire = [st, w, h, fmt, thr](FiringContext& ctx) {
+    if (!st->h) check(df_motion_create(ctx.device(), w, h, fmt, static_cast<std::uint8_t>(thr), &st->h));
+    // inputs: src, delay; outputs: delay, sink (declaration order)
+    check(df_motion_fire_channels(st->h, ctx.input(0), ctx.input(1), ctx.output(1), ctx.stream()));
+  };
+  actors.push_back({"motion",
+                    ActorKind::static_rate,
+                    {{PortDirection::input, PortKind::regular, "src_motion"},
+                     {PortDirection::input, PortKind::regular, "motion_delay"},
+                     {PortDirection::output, PortKind::regular, "motion_delay"},
+                     {PortDirection::output, PortKind::regular, "motion_sink"}},
+                    std::move(fused)});
+
+  ActorBehavior sink;  // motion.cpp:178-183
+  sink.fire = [output, px, r](FiringContext& ctx) {
+    df_region reg;
+    check(df_channel_read_start(ctx.input(0), r, &reg));
+    check(df_memcpy_d2h(output.data() + ctx.firing_index() * r * px, reg.dptr, px * r, ctx.stream()));
+    check(df_channel_read_end(ctx.input(0), &reg, ctx.stream()));
+  };
+  actors.push_back({"sink", ActorKind::static_rate, {{PortDirection::input, PortKind::regular, "motion_sink"}},
+                    std::move(sink)});
+  return df::build_network(std::move(actors), std::move(channels));
+}
+
+}  // namespace df::motion

@@ -1,0 +1,71 @@
+"""ctypes binding of libdf_host.so (include/df_host.h): the C++ GPU-actor
+runtime running the reference's two networks end to end from host buffers."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import _lib
+
+HOST_LIB_PATH = os.path.join(_lib.HERE, "libdf_host.so")
+_h = None
+
+
+class HostRunError(RuntimeError):
+    pass
+
+
+def lib():
+    global _h
+    if _h is None:
+        _lib.lib()  # libdf_cuda.so first (libdf_host.so links it via $ORIGIN)
+        if not os.path.exists(HOST_LIB_PATH):
+            raise RuntimeError(f"{HOST_LIB_PATH} missing: run __graft_entry__.build()")
+        L = C.CDLL(HOST_LIB_PATH)
+        L.dfh_last_error.restype = C.c_char_p
+        L.dfh_dpd_run.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_void_p,
+                                  C.c_void_p, C.c_size_t, C.c_uint32, C.POINTER(C.c_double),
+                                  C.POINTER(C.c_uint64)]
+        L.dfh_motion_run.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint, C.c_uint, C.c_int,
+                                     C.c_uint8, C.c_uint32, C.POINTER(C.c_double), C.POINTER(C.c_uint64)]
+        L.dfh_validate_demo.argtypes = [C.c_int]
+        _h = L
+    return _h
+
+
+def _check(rc):
+    if rc != 0:
+        raise HostRunError(f"[{rc}] {lib().dfh_last_error().decode(errors='replace')}")
+
+
+def dpd_run(inp: np.ndarray, taps: np.ndarray, schedule, period: int, batch: int = 1, device: int = 0,
+            out: np.ndarray | None = None):
+    """run(dpd::build_network(params)) on the GPU; returns (output, sink_active_ms, dpd_firings)."""
+    inp = np.ascontiguousarray(inp, np.float32).reshape(-1)
+    taps = np.ascontiguousarray(taps, np.float32)
+    T = taps.shape[1]
+    sched = np.ascontiguousarray(np.asarray(schedule, np.uint16))
+    out = np.empty_like(inp) if out is None else out
+    ms, fir = C.c_double(0), C.c_uint64(0)
+    _check(lib().dfh_dpd_run(device, inp.ctypes.data_as(C.c_void_p), out.ctypes.data_as(C.c_void_p), inp.size // 2,
+                             period, T, taps.ctypes.data_as(C.c_void_p), sched.ctypes.data_as(C.c_void_p),
+                             sched.size, batch, C.byref(ms), C.byref(fir)))
+    return out, ms.value, fir.value
+
+
+def motion_run(frames: np.ndarray, width: int, height: int, fmt: int = 1, threshold: int = 32, rate: int = 1,
+               device: int = 0, out: np.ndarray | None = None):
+    """run(motion::build_network(params)) on the GPU; returns (masks, sink_active_ms, delay_tokens_written)."""
+    frames = np.ascontiguousarray(frames, np.uint8).reshape(-1)
+    n = frames.size // (width * height * fmt)
+    out = np.empty(n * width * height, np.uint8) if out is None else out
+    ms, dw = C.c_double(0), C.c_uint64(0)
+    _check(lib().dfh_motion_run(device, frames.ctypes.data_as(C.c_void_p), out.ctypes.data_as(C.c_void_p), n, width,
+                                height, fmt, threshold, rate, C.byref(ms), C.byref(dw)))
+    return out, ms.value, dw.value
+
+
+def validate_demo(which: int) -> int:
+    return int(lib().dfh_validate_demo(which))

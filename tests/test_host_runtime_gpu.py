@@ -1,0 +1,60 @@
+"""GPU: the C++ GPU-actor runtime (static schedule, per-actor streams,
+event-encoded channel protocol, device-resident token counts) runs the
+reference's two networks from host buffers and matches the oracle."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_1611_03226_b200 import host_api as H
+
+pytestmark = pytest.mark.gpu
+
+
+def bits(a):
+    return np.ascontiguousarray(a, np.float32).view(np.uint32)
+
+
+@pytest.mark.parametrize("period,batch,blocks", [(256, 1, 8), (256, 4, 16), (4096, 8, 64), (64, 3, 21), (4, 5, 40)])
+def test_dpd_network_equals_oracle(gpu, period, batch, blocks):
+    x = O.synth_samples(period * blocks, 43)
+    taps = O.random_taps(41)
+    sched = O.random_schedule(5, 42)
+    sched[1] = 1  # a single-branch block (extension; the oracle accepts it)
+    got, ms, firings = H.dpd_run(x, taps, sched, period, batch)
+    assert firings == blocks // batch
+    np.testing.assert_array_equal(bits(got), bits(O.dpd(x, taps, sched, period)))
+
+
+def test_dpd_network_t32(gpu):
+    x = O.synth_samples(1024 * 16, 5)
+    taps = O.random_taps(7, 32)
+    got, _, _ = H.dpd_run(x, taps, [0x3FF], 1024, 4)
+    np.testing.assert_array_equal(bits(got), bits(O.dpd(x, taps, [0x3FF], 1024)))
+
+
+def test_dpd_network_rejects_bad_schedule(gpu):
+    x = O.synth_samples(256, 1)
+    with pytest.raises(H.HostRunError, match="invalid_argument"):
+        H.dpd_run(x, O.random_taps(1), [0x7FF], 64)  # branch 11 (check_config)
+    with pytest.raises(H.HostRunError, match="invalid_argument"):
+        H.dpd_run(x, O.random_taps(1), [3], 48)  # samples not a multiple of period
+
+
+@pytest.mark.parametrize("rate", [1, 4, 7])
+@pytest.mark.parametrize("fmt", [1, 3])
+def test_motion_network_equals_oracle(gpu, rate, fmt):
+    w, h, n = 64, 48, 28
+    f = O.synth_bytes(n * w * h * fmt, 2024)
+    got, ms, delay_written = H.motion_run(f, w, h, fmt, 32, rate)
+    want = O.motion_rgb(f, w, h) if fmt == 3 else O.motion_gray(f, w, h)
+    np.testing.assert_array_equal(got, want)
+    assert delay_written == n // rate  # one delay token per firing through the self-loop
+
+
+def test_motion_acceptance6_through_runtime(gpu, hashes):
+    import hashlib
+    h = hashes["motion_acceptance6"]
+    f = O.synth_bytes(h["frames"] * h["w"] * h["h"], h["seed"])
+    for rate in (1, 4):
+        got, _, _ = H.motion_run(f, h["w"], h["h"], 1, h["thr"], rate)
+        assert hashlib.sha256(got.tobytes()).hexdigest() == h["out_sha256"]
