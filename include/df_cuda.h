@@ -168,6 +168,12 @@ int df_dpd_reset(df_dpd* dpd, void* stream); /* zero FIR history */
 /* Reads the FIR history (10 branches x (T-1) complex) to host; synchronizes. */
 int df_dpd_get_state(df_dpd* dpd, float* state_host);
 int df_dpd_error(df_dpd* dpd); /* sticky device error word; synchronizes */
+/* Sets the FIR history of every branch in branch_mask from `count` raw
+ * input samples preceding the next firing (interleaved, device): exactly
+ * the state fir10 leaves after processing them (dpd.cpp:108-120) --
+ * poly recomputed, older history kept when count < T-1.  This is the
+ * FIR-history halo of a block-range shard. */
+int df_dpd_set_history(df_dpd* dpd, const float* raw_dev, uint32_t count, uint32_t branch_mask, void* stream);
 /* Batched firing on raw device buffers: `blocks` consecutive firings, block
  * i governed by ctrl_dev[i] (uint32 LE) and reading/writing samples
  * [i*period, (i+1)*period) of in_dev / out_dev.  Equivalent to `blocks`

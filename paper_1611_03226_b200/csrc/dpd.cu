@@ -389,6 +389,24 @@ __global__ void dpd_main_generic_kernel(DpdIO io, const float2* __restrict__ tap
   }
 }
 
+// History from raw halo samples: branch b's state[j] = poly_b(raw[count-1-j])
+// (older state kept for j >= count), as fir10 would leave it.
+__global__ void dpd_set_history_kernel(float2* state, const float2* __restrict__ raw, unsigned count,
+                                       unsigned mask, int T) {
+  const int b = blockIdx.x + 1;
+  if (!((mask >> (b - 1)) & 1u)) return;
+  const int H1 = T - 1;
+  float2* st = state + (size_t)blockIdx.x * (kMaxTaps - 1);
+  __shared__ float2 old[kMaxTaps];
+  if ((int)threadIdx.x < H1) old[threadIdx.x] = st[threadIdx.x];
+  __syncthreads();
+  const int j = threadIdx.x;
+  if (j < H1) {
+    const long long idx = (long long)count - 1 - j;
+    st[j] = idx >= 0 ? poly_sample(raw[idx].x, raw[idx].y, b) : old[-idx - 1];
+  }
+}
+
 __global__ void dpd_config_kernel(const uint16_t* __restrict__ sched, unsigned len,
                                   unsigned long long first, unsigned long long count,
                                   uint32_t* __restrict__ ctrl) {
@@ -581,6 +599,17 @@ int df_dpd_error(df_dpd* d) {
   if (err == DF_ECONTROL) return set_error(DF_ECONTROL, "config token names a branch beyond 10");
   if (err) return set_error((int)err, "dpd: device error %u", err);
   return DF_OK;
+}
+
+int df_dpd_set_history(df_dpd* d, const float* raw_dev, uint32_t count, uint32_t branch_mask, void* stream) {
+  DF_REQUIRE(d, DF_EINVAL, "df_dpd_set_history: null actor");
+  DF_REQUIRE(branch_mask >> kBranches == 0, DF_ECONTROL, "config token names a branch beyond 10");
+  if (d->T <= 1 || count == 0 || branch_mask == 0) return DF_OK;
+  DF_REQUIRE(raw_dev, DF_EINVAL, "df_dpd_set_history: null samples");
+  DF_CHECK_CUDA(cudaSetDevice(d->device));
+  dpd_set_history_kernel<<<kBranches, 32, 0, as_stream(stream)>>>(d->state, reinterpret_cast<const float2*>(raw_dev),
+                                                                   count, branch_mask, (int)d->T);
+  return after_launch("dpd_set_history_kernel");
 }
 
 int df_dpd_fire(df_dpd* d, const uint32_t* ctrl_dev, const float* in_dev, float* out_dev,

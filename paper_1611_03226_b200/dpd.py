@@ -65,6 +65,12 @@ class DpdActor:
         call("df_dpd_get_state", self.handle, out.ctypes.data_as(C.c_void_p))
         return out[: BRANCHES * (self.T - 1) * 2].reshape(BRANCHES, self.T - 1, 2)
 
+    def set_history(self, raw: Buffer, count: int, branch_mask: int = 0x3FF, stream: Stream | None = None,
+                    offset: int = 0):
+        """FIR-history halo: state as left by processing `count` raw samples."""
+        call("df_dpd_set_history", self.handle, raw.at(offset), int(count), int(branch_mask),
+             stream.handle if stream else None)
+
     def check(self):
         call("df_dpd_error", self.handle)
 

@@ -1,0 +1,51 @@
+"""Multi-GPU decomposition of the two workloads: independent
+frame-range / block-range shards with one-frame / FIR-history halos,
+exchanged point to point between neighbouring ranks -- no collective on
+the data path.  The exchange helpers take torch tensors so the same code
+runs over NCCL (CUDA tensors, the bench) and gloo (CPU tensors, tests)."""
+from __future__ import annotations
+
+
+def even_ranges(total: int, world: int, align: int = 1) -> list[tuple[int, int]]:
+    """Contiguous [start, end) ranges, sizes multiples of `align` (except the last)."""
+    units = -(-total // align)
+    out = []
+    for r in range(world):
+        a = units * r // world * align
+        b = min(total, units * (r + 1) // world * align)
+        out.append((a, b))
+    return out
+
+
+def frame_shards(frames: int, world: int) -> list[tuple[int, int]]:
+    return even_ranges(frames, world)
+
+
+def block_shards(samples: int, period: int, world: int) -> list[tuple[int, int]]:
+    """Sample ranges made of whole blocks (a block is one token)."""
+    return even_ranges(samples, world, period)
+
+
+def dpd_halo_block(schedule, first_block: int, branch: int) -> int | None:
+    """Index of the last block before `first_block` in which `branch` is
+    active (its tail is the branch's FIR history), or None (zero state).
+    The schedule cycles per block (proj/src/dpd.cpp:208)."""
+    for p in range(first_block - 1, -1, -1):
+        if (int(schedule[p % len(schedule)]) >> (branch - 1)) & 1:
+            return p
+    return None
+
+
+def exchange_tail(send_tail, recv_buf, rank: int, world: int):
+    """Rank r sends `send_tail` (its last frame / last T-1 samples) to r+1 and
+    receives r-1's into `recv_buf`.  Returns True if a halo was received."""
+    import torch.distributed as dist
+    ops = []
+    if rank + 1 < world:
+        ops.append(dist.P2POp(dist.isend, send_tail, rank + 1))
+    if rank > 0:
+        ops.append(dist.P2POp(dist.irecv, recv_buf, rank - 1))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    return rank > 0

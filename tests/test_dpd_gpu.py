@@ -204,3 +204,28 @@ def test_channel_bound_firing(gpu):
         assert st.tokens_written == K * rounds and st.tokens_read == K * rounds and st.tokens_available == 0
     a.check()
     assert_parity(got, O.dpd(x, taps, sched, period))
+
+
+def test_block_shard_with_history_halo(gpu):
+    """A block-range shard primed from the T-1 raw samples before it
+    (df_dpd_set_history) equals the matching slice of the full run; for a
+    dynamic schedule each branch takes the tail of its last active block."""
+    from paper_1611_03226_b200 import dpd, shard
+    from paper_1611_03226_b200.device import Buffer
+    for T, sched in [(32, [0x3FF]), (10, list(O.random_schedule(7, 3)) + [1])]:
+        period, blocks, s_block = 128, 16, 9
+        x = O.synth_samples(period * blocks, 8)
+        taps = O.random_taps(9, T)
+        full = O.dpd(x, taps, sched, period)
+        a = dpd.DpdActor(period, taps)
+        xb = Buffer.from_array(x)
+        for b in range(1, 11):
+            hb = shard.dpd_halo_block(sched, s_block, b)
+            if hb is not None:
+                a.set_history(xb, period, 1 << (b - 1), offset=8 * period * hb)
+        rest = blocks - s_block
+        ctrl = Buffer.from_array(np.array([sched[(s_block + i) % len(sched)] for i in range(rest)], np.uint32))
+        out = Buffer(8 * period * rest)
+        a.fire(ctrl, xb, out, rest, in_offset=8 * period * s_block)
+        got = out.download(np.float32)
+        assert_parity(got, full[2 * period * s_block:])
