@@ -397,7 +397,7 @@ __device__ __forceinline__ void frame_pass(const unsigned char* __restrict__ fra
 }
 
 template <int FMT, bool FAST>
-__global__ void __launch_bounds__(32 * kWarpsPerCta) motion_fused_kernel(MotionIO io, MotionGeom g,
+__global__ void __launch_bounds__(32 * kWarpsPerCta, 16) motion_fused_kernel(MotionIO io, MotionGeom g,
                                                                          unsigned* done_counter) {
   extern __shared__ uint2 prev_all[];  // [kWarpsPerCta][(kBandRows + 2) * 32]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
