@@ -87,6 +87,9 @@ __global__ void __launch_bounds__(1024) dpd_prep_kernel(DpdIO io, const float2* 
                                                         int* act, unsigned long long K,
                                                         unsigned period, int T,
                                                         unsigned* err) {
+  // Programmatic dependent launch: the main kernel may start now; only its
+  // block-start tiles (which read the history table) wait for this grid.
+  asm volatile("griddepcontrol.launch_dependents;");
   const int b = blockIdx.x + 1;
   const uint32_t* ctrl = io_ctrl(io);
   const float2* x = io_in(io);
@@ -225,6 +228,7 @@ __global__ void __launch_bounds__(THREADS) dpd_main_kernel(DpdIO io, const float
   float outr[V], outi[V];
 #pragma unroll
   for (int j = 0; j < V; ++j) outr[j] = outi[j] = -0.0f;
+  if (tile == 0) asm volatile("griddepcontrol.wait;" ::: "memory");  // history table from prep
   int prev_b = 1;
   int buf = 0;
 #pragma unroll 1
@@ -311,6 +315,9 @@ __global__ void __launch_bounds__(THREADS) dpd_main_kernel(DpdIO io, const float
     st[pad_index(tid * V + j)] = make_float2(__fadd_rn(outr[j], 0.0f), __fadd_rn(outi[j], 0.0f));
   __syncthreads();
   for (int o = tid; o < n; o += THREADS) y[blk + t0 + o] = st[pad_index(o)];
+  // Never complete before the prep grid (it also advances the FirState the
+  // next batch's prep reads).
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (io.channel_mode) {
     // Last CTA commits the firing batch: K control tokens, K block tokens
@@ -485,11 +492,22 @@ int launch_dpd(df_dpd* d, const DpdIO& io, unsigned long long K, cudaStream_t s)
         DF_REQUIRE(K <= 65535, DF_EINVAL, "dpd: channel firing batch > 65535");
       }
       const float2* hist = d->hist + base * kBranches * (d->T - 1);
-      dim3 grid(tiles, (unsigned)k);
-      if (d->T == 10)
-        dpd_main_kernel<10, kV, kThreads><<<grid, kThreads, 0, s>>>(sub, d->taps, hist, d->period, tiles, err, done);
-      else
-        dpd_main_kernel<32, kV, kThreads><<<grid, kThreads, 0, s>>>(sub, d->taps, hist, d->period, tiles, err, done);
+      cudaLaunchConfig_t lc{};
+      lc.gridDim = dim3(tiles, (unsigned)k);
+      lc.blockDim = dim3(kThreads);
+      lc.dynamicSmemBytes = 0;
+      lc.stream = s;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      lc.attrs = attr;
+      lc.numAttrs = 1;
+      cudaError_t le = d->T == 10
+                           ? cudaLaunchKernelEx(&lc, dpd_main_kernel<10, kV, kThreads>, sub, (const float2*)d->taps,
+                                                hist, d->period, tiles, err, done)
+                           : cudaLaunchKernelEx(&lc, dpd_main_kernel<32, kV, kThreads>, sub, (const float2*)d->taps,
+                                                hist, d->period, tiles, err, done);
+      DF_CHECK_CUDA(le);
       DF_TRY(after_launch("dpd_main_kernel"));
     }
   } else {
