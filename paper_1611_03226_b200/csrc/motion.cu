@@ -40,7 +40,13 @@
 namespace df {
 namespace {
 
-constexpr int kBandRows = 48;             // R
+#ifndef DF_MOTION_R
+#define DF_MOTION_R 48
+#endif
+#ifndef DF_MOTION_MINB
+#define DF_MOTION_MINB 14
+#endif
+constexpr int kBandRows = DF_MOTION_R;    // R (A/B: profiles/r01_ab_motion_variants.txt)
 constexpr int kWarpsPerCta = 1;  // y0 depends on blockIdx only: warp-uniform for the compiler
 constexpr int kPxPerLane = 8;
 constexpr int kOutPxPerWarp = 30 * kPxPerLane;  // 240
@@ -397,7 +403,7 @@ __device__ __forceinline__ void frame_pass(const unsigned char* __restrict__ fra
 }
 
 template <int FMT, bool FAST>
-__global__ void __launch_bounds__(32 * kWarpsPerCta, 16) motion_fused_kernel(MotionIO io, MotionGeom g,
+__global__ void __launch_bounds__(32 * kWarpsPerCta, DF_MOTION_MINB) motion_fused_kernel(MotionIO io, MotionGeom g,
                                                                          unsigned* done_counter) {
   extern __shared__ uint2 prev_all[];  // [kWarpsPerCta][(kBandRows + 2) * 32]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
