@@ -422,8 +422,14 @@ __global__ void dpd_config_kernel(const uint16_t* __restrict__ sched, unsigned l
     ctrl[i] = sched[(first + i) % len];  // LE 4-byte wire form (dpd.hpp:38-41)
 }
 
-constexpr int kV = 8;
-constexpr int kThreads = 128;
+#ifndef DF_DPD_V
+#define DF_DPD_V 8
+#endif
+#ifndef DF_DPD_THREADS
+#define DF_DPD_THREADS 128
+#endif
+constexpr int kV = DF_DPD_V;              // consecutive outputs per thread
+constexpr int kThreads = DF_DPD_THREADS;  // threads per CTA (tile = kV * kThreads samples)
 
 }  // namespace
 }  // namespace df

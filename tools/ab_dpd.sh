@@ -1,0 +1,15 @@
+#!/bin/bash
+cd "$(dirname "$0")/.."
+mkdir -p gpurun_out
+: > gpurun_out/ab.txt
+for rep in 1 2; do
+for v in paper_1611_03226_b200/variants/*.so; do
+  for w in dpd1 dpd3 dpd5; do
+    r=$(DF_CUDA_LIB=$PWD/$v timeout 300 python bench.py --workload $w --steps 10 --warmup 3 --no-cpu-baseline --no-secondary 2>/dev/null | python -c "import json,sys; d=json.load(sys.stdin); print(d['ms_per_step'], d['roofline']['frac'])")
+    echo "$(basename $v) $w $r" >> gpurun_out/ab.txt
+  done
+done
+done
+for v in paper_1611_03226_b200/variants/*.so; do
+  echo "$(basename $v): $(DF_CUDA_LIB=$PWD/$v timeout 300 python -m pytest tests/test_dpd_gpu.py -q -x 2>&1 | tail -1)" >> gpurun_out/ab_tests.txt
+done
