@@ -43,6 +43,9 @@ namespace {
 #ifndef DF_MOTION_R
 #define DF_MOTION_R 48
 #endif
+#ifndef DF_MOTION_PF
+#define DF_MOTION_PF 8
+#endif
 #ifndef DF_MOTION_MINB
 #define DF_MOTION_MINB 14
 #endif
@@ -73,6 +76,7 @@ struct MotionGeom {
   unsigned wh[8];    // horizontal gauss
 };
 
+
 __device__ __forceinline__ unsigned dp4a(unsigned a, unsigned b, unsigned c) {
   return __dp4a(a, b, c);
 }
@@ -101,6 +105,12 @@ __device__ __forceinline__ unsigned lop_sel(unsigned s, unsigned a, unsigned b) 
   unsigned d;
   asm("lop3.b32 %0, %1, %2, %3, 0xE2;" : "=r"(d) : "r"(a), "r"(s), "r"(b));
   return d;
+}
+
+__device__ __forceinline__ uint2 ldg_pinned(const unsigned char* p) {
+  uint2 v;
+  asm volatile("ld.global.nc.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+  return v;
 }
 
 constexpr unsigned W8(unsigned a, unsigned b, unsigned c, unsigned d) {
@@ -180,6 +190,7 @@ struct RowSlot {
   uint2 raw[FMT == DF_MOTION_RGB ? 3 : 1];  // prefetched input of row (this + 5)
   int raw_y;       // row index of raw (uniform)
 };
+
 
 // Issues the loads of row y into r.raw (FAST: aligned vector loads; the
 // values are consumed five rows later).  The row index is clamped into the
@@ -295,7 +306,11 @@ __device__ __forceinline__ void column_masks(int x, int W, unsigned gm[2], unsig
 // Processes one frame for this warp's (tile, band).  MODE 0: gauss only,
 // into the prev buffer (warm-up of a frame range).  MODE 1: full chain.
 // MODE 2: full chain + writes the next delay token (last frame of a firing).
-template <int FMT, bool FAST, int MODE>
+// INT: interior band (FAST only) -- every row the pass touches, including
+// the 5-row-ahead prefetch, lies inside the frame and no gauss/median row is
+// a border row, so the pass runs with pointer-increment addressing and no
+// row clamps, lane zeroing or border tests (interior_band()).
+template <int FMT, bool FAST, int MODE, bool INT>
 __device__ __forceinline__ void frame_pass(const unsigned char* __restrict__ frame,
                                            unsigned char* __restrict__ out,
                                            unsigned char* __restrict__ next_tok,
@@ -303,16 +318,53 @@ __device__ __forceinline__ void frame_pass(const unsigned char* __restrict__ fra
                                            uint2* __restrict__ prev_s, const MotionGeom& g, int y0,
                                            int x, int xc, bool lane_in, int lane, const unsigned gm[2],
                                            const unsigned mm[2]) {
+  static_assert(!INT || FAST, "interior passes need aligned 8-px segments");
   const int W = g.W, H = g.H;
   const bool out_lane = lane >= 1 && lane <= 30;
   const unsigned row_bytes = (unsigned)W * FMT;  // a frame is < 4 GiB (checked at create)
   const unsigned lane_off = (unsigned)xc * FMT;
   RowSlot<FMT> s[5];
+  // INT: next row to prefetch, next output row, next prev_s row.
+  const unsigned char* fptr = INT ? frame + ((size_t)(unsigned)(y0 - 3) * row_bytes + lane_off) : nullptr;
+  unsigned ooff = (unsigned)y0 * (unsigned)W + (unsigned)x;  // INT: next output row (a frame is < 4 GiB)
+
+  auto fetch = [&](RowSlot<FMT>& r, int y) {
+    if (INT) {
+      // volatile: keeps each row's loads in its own step (5 rows ahead of
+      // use) instead of being sunk to the loop latch.
+      r.raw[0] = ldg_pinned(fptr);
+      if (FMT == DF_MOTION_RGB) {
+        r.raw[1] = ldg_pinned(fptr + 8);
+        r.raw[2] = ldg_pinned(fptr + 16);
+      }
+      fptr += row_bytes;
+      if (DF_MOTION_PF > 0) {
+        // L2 prefetch DF_MOTION_PF rows further (clamped into the frame):
+        // more bytes in flight than the five register-held rows allow.
+        const unsigned yp = (unsigned)min(y + DF_MOTION_PF, H - 1);
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(frame + ((size_t)yp * row_bytes + lane_off)));
+      }
+    } else {
+      fetch_row<FMT, FAST>(r, frame, lane_off, y, H, row_bytes);
+    }
+  };
 
   auto produce = [&](RowSlot<FMT>& r, int gy) {
     unsigned g0, g1;
-    convert_row<FMT, FAST>(r, frame, x, lane_in, W, H, g0, g1, g.wg);
-    fetch_row<FMT, FAST>(r, frame, lane_off, gy + 5, H, row_bytes);  // rows past the band are harmless
+    if (INT) {
+      // Out-of-frame lanes (x < 0 or x >= W) read a clamped column; their
+      // values only reach gauss/median border columns, which are copied.
+      if (FMT == DF_MOTION_RGB) {
+        g0 = rgb4_to_gray(r.raw[0].x, r.raw[0].y, r.raw[1].x, g.wg);
+        g1 = rgb4_to_gray(r.raw[1].y, r.raw[2].x, r.raw[2].y, g.wg);
+      } else {
+        g0 = r.raw[0].x;
+        g1 = r.raw[0].y;
+      }
+    } else {
+      convert_row<FMT, FAST>(r, frame, x, lane_in, W, H, g0, g1, g.wg);
+    }
+    fetch(r, gy + 5);  // rows past the band are harmless
     const unsigned left = __shfl_up_sync(0xffffffffu, g1, 1);
     const unsigned right = __shfl_down_sync(0xffffffffu, g0, 1);
     hgauss4(left, g0, g1, r.h[0], r.h[1], g.wh);
@@ -321,11 +373,12 @@ __device__ __forceinline__ void frame_pass(const unsigned char* __restrict__ fra
     r.g[1] = g1;
   };
 
-  // gauss + thres of row gc = gy - 2 (window r4..r0 = rows gy-4..gy).
+  // gauss + thres of row gc = gy - 2 (window r4..r0 = rows gy-4..gy); ps is
+  // the prev_s slot of row gc.
   auto gauss_thres = [&](RowSlot<FMT>& r4, RowSlot<FMT>& r3, RowSlot<FMT>& r2, RowSlot<FMT>& r1,
-                         RowSlot<FMT>& r0, int gc) {
+                         RowSlot<FMT>& r0, int gc, uint2* ps) {
     unsigned gw[2];
-    if ((unsigned)(gc - 2) >= (unsigned)(H - 4)) {  // gc < 2 || gc >= H-2: gray copied
+    if (!INT && (unsigned)(gc - 2) >= (unsigned)(H - 4)) {  // gc < 2 || gc >= H-2: gray copied
       gw[0] = r2.g[0];
       gw[1] = r2.g[1];
     } else {
@@ -337,7 +390,6 @@ __device__ __forceinline__ void frame_pass(const unsigned char* __restrict__ fra
         gw[w] = lop_sel(gm[w], r2.g[w], prmt(v0, v1, 0x7531));
       }
     }
-    uint2* ps = prev_s + (gc - (y0 - 1)) * 32 + lane;
     if (MODE == 0) {
       *ps = make_uint2(gw[0], gw[1]);
       return;
@@ -358,7 +410,7 @@ __device__ __forceinline__ void frame_pass(const unsigned char* __restrict__ fra
     const unsigned lnb = __shfl_up_sync(0xffffffffu, c1, 1);
     const unsigned rnb = __shfl_down_sync(0xffffffffu, c0, 1);
     unsigned o0, o1;
-    if ((unsigned)(m - 1) >= (unsigned)(H - 2)) {  // m == 0 || m == H-1: copied
+    if (!INT && (unsigned)(m - 1) >= (unsigned)(H - 2)) {  // m == 0 || m == H-1: copied
       o0 = c0;
       o1 = c1;
     } else {
@@ -367,7 +419,14 @@ __device__ __forceinline__ void frame_pass(const unsigned char* __restrict__ fra
       o0 = lop_sel(mm[0], c0, maj5(c0, r4.t[0], r2.t[0], l0, r0w));
       o1 = lop_sel(mm[1], c1, maj5(c1, r4.t[1], r2.t[1], l1, r1w));
     }
-    if (out_lane) store_bytes8<FAST>(out, m, x, W, prmt(o0, 0, 0xBA98), prmt(o1, 0, 0xBA98));
+    o0 = prmt(o0, 0, 0xBA98);
+    o1 = prmt(o1, 0, 0xBA98);
+    if (INT) {
+      if (out_lane && x < W) *reinterpret_cast<uint2*>(out + ooff) = make_uint2(o0, o1);
+      ooff += (unsigned)W;
+    } else if (out_lane) {
+      store_bytes8<FAST>(out, m, x, W, o0, o1);
+    }
   };
 
   // One step per gauss row gc (y0-1 .. gc_end): window rows gc-2..gc+2 are
@@ -375,17 +434,21 @@ __device__ __forceinline__ void frame_pass(const unsigned char* __restrict__ fra
   // from them and, independently (ILP), produces row gc+3 into the slot of
   // row gc-2 once that row has been consumed.
   const int gc_end = min(y0 + kBandRows, H);  // last gauss row needed
+  // INT: the last produce (row y0+R+3) is surplus but in-frame, and the
+  // break per step keeps ptxas scheduling step by step (each row's loads
+  // stay five rows ahead of their use; a fixed-trip unrolled loop let it sink
+  // all loads to the latch -- profiles/r01_ab_motion_variants.txt).
   auto step = [&](RowSlot<FMT>& r4, RowSlot<FMT>& r3, RowSlot<FMT>& r2, RowSlot<FMT>& r1, RowSlot<FMT>& r0,
                   int gc) {
     // r4..r0 = rows gc-2 .. gc+2
-    gauss_thres(r4, r3, r2, r1, r0, gc);
+    gauss_thres(r4, r3, r2, r1, r0, gc, prev_s + (gc - (y0 - 1)) * 32 + lane);
     if (MODE != 0 && gc > y0) median(r4, r3, r2, gc - 1);  // rows gc-2, gc-1, gc
-    if (gc < gc_end) produce(r4, gc + 3);
+    if (INT || gc < gc_end) produce(r4, gc + 3);
   };
 
   int gc = y0 - 1;
 #pragma unroll
-  for (int k = 0; k < 5; ++k) fetch_row<FMT, FAST>(s[k], frame, lane_off, y0 - 3 + k, H, row_bytes);
+  for (int k = 0; k < 5; ++k) fetch(s[k], y0 - 3 + k);
 #pragma unroll
   for (int k = 0; k < 5; ++k) produce(s[k], y0 - 3 + k);
   while (true) {
@@ -402,6 +465,44 @@ __device__ __forceinline__ void frame_pass(const unsigned char* __restrict__ fra
   }
 }
 
+// A band is interior when every row a pass reads (y0-3 .. y0+R+2, plus the
+// prefetch of rows up to y0+R+8) is inside the frame and no gauss row
+// (y0-1 .. y0+R) or median row (y0 .. y0+R-1) is a border row.
+__device__ __forceinline__ bool interior_band(int y0, int H) {
+  return y0 >= 3 && y0 + kBandRows + 8 <= H - 1;
+}
+
+template <int FMT, bool FAST, bool INT>
+__device__ __forceinline__ void walk_frames(const MotionIO& io, const unsigned char* in, unsigned char* out,
+                                            const unsigned char* prev_tok, unsigned char* next_tok,
+                                            unsigned char* next_copy, uint2* prev_s, const MotionGeom& g,
+                                            int y0, int x, int xc, bool lane_in, int lane, int f_begin,
+                                            int f_end) {
+  const size_t in_frame = (size_t)g.W * g.H * FMT;
+  const size_t frame_px = (size_t)g.W * g.H;
+  unsigned gm[2], mm[2];
+  column_masks(x, g.W, gm, mm);
+  if (f_begin == 0) {
+    // Delay token: gauss of the previous firing's last frame.
+#pragma unroll 10
+    for (int r = 0; r < kBandRows + 2; ++r) {
+      unsigned a0, a1;
+      load_bytes8<FAST>(prev_tok, y0 - 1 + r, x, g.W, g.H, a0, a1);
+      prev_s[r * 32 + lane] = make_uint2(a0, a1);
+    }
+  } else {
+    frame_pass<FMT, FAST, 0, INT>(in + (size_t)(f_begin - 1) * in_frame, nullptr, nullptr, nullptr, prev_s, g,
+                                  y0, x, xc, lane_in, lane, gm, mm);
+  }
+  const int f_last = (f_end == g.frames) ? f_end - 1 : f_end;  // frame that emits the delay token
+  for (int f = f_begin; f < f_last; ++f)
+    frame_pass<FMT, FAST, 1, INT>(in + (size_t)f * in_frame, out + (size_t)f * frame_px, nullptr, nullptr,
+                                  prev_s, g, y0, x, xc, lane_in, lane, gm, mm);
+  if (f_last < f_end)
+    frame_pass<FMT, FAST, 2, INT>(in + (size_t)f_last * in_frame, out + (size_t)f_last * frame_px, next_tok,
+                                  next_copy, prev_s, g, y0, x, xc, lane_in, lane, gm, mm);
+}
+
 template <int FMT, bool FAST>
 __global__ void __launch_bounds__(32 * kWarpsPerCta, DF_MOTION_MINB) motion_fused_kernel(MotionIO io, MotionGeom g,
                                                                          unsigned* done_counter) {
@@ -414,9 +515,6 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, DF_MOTION_MINB) motion_fuse
   const int xc = lane_in ? x : 0;
   const int f_begin = blockIdx.z * g.chunk;
   const int f_end = min(f_begin + g.chunk, g.frames);
-  const size_t in_frame = (size_t)g.W * g.H * FMT;
-  const size_t frame_px = (size_t)g.W * g.H;
-
   const unsigned char* in = io.in;
   unsigned char* out = io.out;
   const unsigned char* prev_tok = io.prev;
@@ -432,27 +530,12 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, DF_MOTION_MINB) motion_fuse
 
   if (y0 < g.H && f_begin < f_end) {
     uint2* prev_s = prev_all + warp * (kBandRows + 2) * 32;
-    unsigned gm[2], mm[2];
-    column_masks(x, g.W, gm, mm);
-    if (f_begin == 0) {
-      // Delay token: gauss of the previous firing's last frame.
-#pragma unroll 10
-      for (int r = 0; r < kBandRows + 2; ++r) {
-        unsigned a0, a1;
-        load_bytes8<FAST>(prev_tok, y0 - 1 + r, x, g.W, g.H, a0, a1);
-        prev_s[r * 32 + lane] = make_uint2(a0, a1);
-      }
-    } else {
-      frame_pass<FMT, FAST, 0>(in + (size_t)(f_begin - 1) * in_frame, nullptr, nullptr, nullptr, prev_s, g,
-                               y0, x, xc, lane_in, lane, gm, mm);
-    }
-    const int f_last = (f_end == g.frames) ? f_end - 1 : f_end;  // frame that emits the delay token
-    for (int f = f_begin; f < f_last; ++f)
-      frame_pass<FMT, FAST, 1>(in + (size_t)f * in_frame, out + (size_t)f * frame_px, nullptr, nullptr, prev_s,
-                               g, y0, x, xc, lane_in, lane, gm, mm);
-    if (f_last < f_end)
-      frame_pass<FMT, FAST, 2>(in + (size_t)f_last * in_frame, out + (size_t)f_last * frame_px, next_tok,
-                               next_copy, prev_s, g, y0, x, xc, lane_in, lane, gm, mm);
+    if (FAST && interior_band(y0, g.H))
+      walk_frames<FMT, FAST, FAST>(io, in, out, prev_tok, next_tok, next_copy, prev_s, g, y0, x, xc, lane_in,
+                                   lane, f_begin, f_end);
+    else
+      walk_frames<FMT, FAST, false>(io, in, out, prev_tok, next_tok, next_copy, prev_s, g, y0, x, xc, lane_in,
+                                    lane, f_begin, f_end);
   }
 
   if (io.channel_mode) {

@@ -78,6 +78,30 @@ def test_rgb_input(gpu, w, h):
     assert_frames_equal(run_gpu(rgb, w, h, fmt=3), O.motion_rgb(rgb, w, h), w, h)
 
 
+@pytest.mark.parametrize("w,h,fmt", [(256, 300, 1), (264, 170, 1), (1280, 200, 3), (488, 240, 3), (96, 117, 3)])
+def test_interior_bands_vs_oracle(gpu, w, h, fmt):
+    # Frames tall enough that most bands take the interior pass (fixed trip
+    # count, no row clamps), next to the general pass of the border bands.
+    n = 4
+    f = O.synth_bytes(n * w * h * fmt, 3 * w + h)
+    want = O.motion_rgb(f, w, h) if fmt == 3 else O.motion_gray(f, w, h)
+    assert_frames_equal(run_gpu(f, w, h, fmt=fmt), want, w, h)
+
+
+def test_interior_bands_temporal_chunks_structured(gpu):
+    # Structured motion (thresholds bite) over many frames: frame-range
+    # warm-up passes (MODE 0) and delay-token passes (MODE 2) in interior bands.
+    w, h, n = 512, 264, 41
+    yy, xx = np.mgrid[0:h, 0:w]
+    frames = np.stack([((xx * 5 + yy * 3 + 11 * t) % 251) for t in range(n)]).astype(np.uint8)
+    frames[7, 60:140, 100:300] = 255
+    frames[20, 100:101, :] = 0
+    want = O.motion_gray(frames.reshape(-1), w, h, 40)
+    assert_frames_equal(run_gpu(frames.reshape(-1), w, h, 40), want, w, h)
+    for chunk in (3, 17):
+        assert_frames_equal(run_gpu(frames.reshape(-1), w, h, 40, chunk=chunk), want, w, h)
+
+
 def test_many_frames_temporal_chunks(gpu):
     # Enough frames that the kernel splits the firing into frame ranges,
     # each recomputing gauss(f0 - 1) on chip.
