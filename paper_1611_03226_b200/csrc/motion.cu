@@ -30,7 +30,12 @@
 // not start the firing recompute gauss(f0-1) once.  No __syncthreads: warps
 // are independent; neighbours are exchanged with shuffles.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include "channel_dev.cuh"
 #include "channel_host.hpp"
@@ -559,6 +564,371 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, DF_MOTION_MINB) motion_fuse
 
 constexpr size_t kSmemBytes = sizeof(uint2) * kWarpsPerCta * (kBandRows + 2) * 32;
 
+// ===========================================================================
+// M3: TMA-fed rows, TMEM-resident delay band.
+//
+// The register-prefetch kernel above is bound by bytes in flight (5 rows per
+// warp in registers, shared memory full with the gauss(prev) bands).  M3
+// moves gauss(prev) into tensor memory (TMEM, 256 KB/SM, otherwise idle:
+// this path has no MMA) and streams the input rows through a per-warp
+// shared-memory ring filled by TMA (cp.async.bulk.tensor, one box of kM3RPS
+// rows per issue, mbarrier completion), kM3Stages * kM3RPS rows ahead of the
+// consumer.  Out-of-frame rows/columns come back zero-filled (OOB) or as a
+// neighbouring frame's rows; both only reach border rows/columns, which the
+// reference copies (motion.cpp:34-37, :64-67).
+//
+// CTA = kM3Warps warps on the same (tile, band), each walking its own frame
+// range (temporal chunk): y0 and x stay warp-uniform, and each warp owns one
+// TMEM lane quarter (warp w -> lanes 32w..32w+31, columns 2r, 2r+1 = prev
+// row r).  The input must be 16-byte row aligned (W*FMT % 16 == 0).
+// ===========================================================================
+#ifndef DF_M3_RPS
+#define DF_M3_RPS 5
+#endif
+#ifndef DF_M3_ST
+#define DF_M3_ST 3
+#endif
+constexpr int kM3Warps = 4;
+// Band heights R (template parameter): a frame pass fetches rows y0-3 ..
+// y0+R+2 (R + 6 rows, whole 5-row boxes), gauss(prev) holds R + 2 rows in
+// 2(R + 2) <= 128 TMEM columns.  launch_m3 picks R per frame geometry.
+template <int R>
+constexpr bool m3_valid_r() { return (R + 6) % 5 == 0 && 2 * (R + 2) <= 128; }
+constexpr int kM3RPS = DF_M3_RPS;
+constexpr int kM3Stages = DF_M3_ST;
+constexpr int kTmemCols = 128;
+static_assert(kM3RPS == 5, "one TMA box per 5-step iteration of the row loop (static in-box row offsets)");
+
+// A TMA box's innermost start must be 16-byte aligned, and a warp tile's
+// row starts 8 bytes past a 16-byte boundary (3 * (240 t - 8) = 720 t - 24
+// RGB, 240 t - 8 gray): each box row is the tile row plus 8 bytes on both
+// sides, and lane l's bytes sit at offset 8 + 8*FMT*l.
+template <int FMT>
+constexpr int m3_row_bytes() { return 32 * kPxPerLane * FMT + 16; }  // 784 / 272 B
+template <int FMT>
+constexpr int m3_stage_bytes() { return (kM3RPS * m3_row_bytes<FMT>() + 127) / 128 * 128; }
+// Dynamic smem: kM3Warps rings (128-B aligned stages for TMA), then the
+// mbarriers, then the TMEM base address slot.
+template <int FMT>
+constexpr size_t m3_ring_bytes() { return (size_t)kM3Stages * m3_stage_bytes<FMT>(); }
+template <int FMT>
+constexpr size_t m3_smem_bytes() {
+  return kM3Warps * m3_ring_bytes<FMT>() + kM3Warps * kM3Stages * 8 + 16;
+}
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+  unsigned done;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tma_load_2d(unsigned dst, const CUtensorMap* map, int c0, int c1, unsigned bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st2(unsigned taddr, unsigned a, unsigned b) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(taddr), "r"(a), "r"(b) : "memory");
+}
+__device__ __forceinline__ void tmem_ld2(unsigned taddr, unsigned& a, unsigned& b) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];" : "=r"(a), "=r"(b) : "r"(taddr) : "memory");
+}
+// The registers of a tcgen05.ld are undefined until wait::ld; tying them to
+// the wait keeps every use after it.
+__device__ __forceinline__ void tmem_wait_ld(unsigned& a, unsigned& b) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(a), "+r"(b)::"memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// Per-warp row stream.  Group g = TMA box g = rows y0-3 + 5*(g % GPP) ..
+// +4 of pass g / GPP (pass P = frame fs + P), in ring stage g % kM3Stages,
+// completing its mbarrier phase (g / kM3Stages) & 1.  The 5-step unrolled
+// row loop consumes exactly one group per iteration, so a row's offset in
+// its box is a compile-time constant.
+template <int FMT, int R>
+struct M3Stream {
+  static_assert(m3_valid_r<R>(), "band height");
+  static constexpr int GPP = (R + 6) / kM3RPS;  // groups per frame pass
+  const CUtensorMap* map;
+  unsigned ring;      // smem address of this warp's ring
+  unsigned bars;      // smem address of this warp's kM3Stages mbarriers
+  unsigned g;         // group being consumed
+  unsigned stage;     // g % kM3Stages
+  unsigned phase;     // (g / kM3Stages) & 1
+  unsigned groups;    // groups in the whole stream
+  unsigned cur;       // this lane's bytes in the current group's first row
+  int c0;             // tensor column (uint32 units) of the warp tile
+  int fs, H, y0;
+  int lane;
+
+  __device__ __forceinline__ void issue(unsigned gi, unsigned s) {  // lane 0 only
+    if (gi >= groups) return;
+    const unsigned pass = gi / GPP;
+    const int row = y0 - 3 + (int)(gi % GPP) * kM3RPS;
+    mbar_expect_tx(bars + 8 * s, kM3RPS * m3_row_bytes<FMT>());
+    tma_load_2d(ring + s * m3_stage_bytes<FMT>(), map, c0, (fs + (int)pass) * H + row, bars + 8 * s);
+  }
+  __device__ __forceinline__ void acquire() {
+    mbar_wait(bars + 8 * stage, phase);
+    cur = ring + stage * m3_stage_bytes<FMT>() + 8 + lane * (kPxPerLane * FMT);
+  }
+  __device__ __forceinline__ unsigned row(int k) const { return cur + k * m3_row_bytes<FMT>(); }
+  // After the group's bytes are in registers (and used): refill its stage
+  // with group g + kM3Stages.
+  __device__ __forceinline__ void release() {
+    __syncwarp();
+    if (lane == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(g + kM3Stages, stage);
+    }
+    ++g;
+    if (++stage == kM3Stages) {
+      stage = 0;
+      phase ^= 1;
+    }
+  }
+};
+
+__device__ __forceinline__ uint2 lds64(unsigned a) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+
+struct M3Row {
+  unsigned h[4];  // horizontal sums, 16x2 packed
+  unsigned g[2];  // gray words
+  unsigned t[2];  // threshold flags
+};
+
+// One frame pass (MODE 0 warm-up / 1 chain / 2 chain + delay token) of the
+// warp's (tile, band).  INT: interior band (no border rows, full R rows).
+template <int FMT, int R, int MODE, bool INT>
+__device__ __forceinline__ void m3_pass(M3Stream<FMT, R>& st, unsigned char* __restrict__ out,
+                                        unsigned char* __restrict__ next_tok, unsigned tmem, const MotionGeom& g,
+                                        int y0, int x, int lane, const unsigned gm[2], const unsigned mm[2]) {
+  const int W = g.W, H = g.H;
+  const bool out_lane = lane >= 1 && lane <= 30;
+  M3Row s[5];
+  unsigned ooff = (unsigned)y0 * (unsigned)W + (unsigned)x;
+  // Each prev row is read (tcgen05.ld, waited) before it is overwritten in
+  // the same step; the previous pass's stores must have landed before this
+  // pass's loads.
+  if (MODE != 0) tmem_wait_st();
+
+  // Row k (0..4) of the current group: the group is acquired at k == 0 and
+  // released at k == 4.
+  auto produce = [&](M3Row& r, int k) {
+    if (k == 0) st.acquire();
+    const unsigned a = st.row(k);
+    unsigned g0, g1;
+    if (FMT == DF_MOTION_RGB) {
+      const uint2 w0 = lds64(a), w1 = lds64(a + 8), w2 = lds64(a + 16);
+      g0 = rgb4_to_gray(w0.x, w0.y, w1.x, g.wg);
+      g1 = rgb4_to_gray(w1.y, w2.x, w2.y, g.wg);
+    } else {
+      const uint2 w0 = lds64(a);
+      g0 = w0.x;
+      g1 = w0.y;
+    }
+    const unsigned left = __shfl_up_sync(0xffffffffu, g1, 1);
+    const unsigned right = __shfl_down_sync(0xffffffffu, g0, 1);
+    hgauss4(left, g0, g1, r.h[0], r.h[1], g.wh);
+    hgauss4(g0, g1, right, r.h[2], r.h[3], g.wh);
+    r.g[0] = g0;
+    r.g[1] = g1;
+    if (k == kM3RPS - 1) st.release();
+  };
+
+  auto gauss_thres = [&](M3Row& r4, M3Row& r3, M3Row& r2, M3Row& r1, M3Row& r0, int gc) {
+    const unsigned ta = tmem + 2u * (unsigned)(gc - (y0 - 1));
+    unsigned p0 = 0, p1 = 0;
+    if (MODE != 0) tmem_ld2(ta, p0, p1);
+    unsigned gw[2];
+    if (!INT && (unsigned)(gc - 2) >= (unsigned)(H - 4)) {  // gc < 2 || gc >= H-2: gray copied
+      gw[0] = r2.g[0];
+      gw[1] = r2.g[1];
+    } else {
+#pragma unroll
+      for (int w = 0; w < 2; ++w) {
+        const unsigned v0 = vgauss(r4.h[2 * w], r3.h[2 * w], r2.h[2 * w], r1.h[2 * w], r0.h[2 * w]);
+        const unsigned v1 =
+            vgauss(r4.h[2 * w + 1], r3.h[2 * w + 1], r2.h[2 * w + 1], r1.h[2 * w + 1], r0.h[2 * w + 1]);
+        gw[w] = lop_sel(gm[w], r2.g[w], prmt(v0, v1, 0x7531));
+      }
+    }
+    if (MODE != 0) {
+      tmem_wait_ld(p0, p1);
+      r2.t[0] = thres4(gw[0], p0, g);
+      r2.t[1] = thres4(gw[1], p1, g);
+    }
+    tmem_st2(ta, gw[0], gw[1]);
+    if (MODE == 2 && out_lane && x < W && gc >= y0 && gc < y0 + R && gc < H)
+      *reinterpret_cast<uint2*>(next_tok + ((unsigned)gc * (unsigned)W + (unsigned)x)) = make_uint2(gw[0], gw[1]);
+  };
+
+  auto median = [&](M3Row& r4, M3Row& r3, M3Row& r2, int m) {
+    const unsigned c0 = r3.t[0], c1 = r3.t[1];
+    const unsigned lnb = __shfl_up_sync(0xffffffffu, c1, 1);
+    const unsigned rnb = __shfl_down_sync(0xffffffffu, c0, 1);
+    unsigned o0, o1;
+    if (!INT && (unsigned)(m - 1) >= (unsigned)(H - 2)) {  // m == 0 || m == H-1: copied
+      o0 = c0;
+      o1 = c1;
+    } else {
+      const unsigned l0 = __funnelshift_l(lnb, c0, 8), r0w = __funnelshift_r(c0, c1, 8);
+      const unsigned l1 = __funnelshift_l(c0, c1, 8), r1w = __funnelshift_r(c1, rnb, 8);
+      o0 = lop_sel(mm[0], c0, maj5(c0, r4.t[0], r2.t[0], l0, r0w));
+      o1 = lop_sel(mm[1], c1, maj5(c1, r4.t[1], r2.t[1], l1, r1w));
+    }
+    if (out_lane && x < W)
+      *reinterpret_cast<uint2*>(out + ooff) = make_uint2(prmt(o0, 0, 0xBA98), prmt(o1, 0, 0xBA98));
+    ooff += (unsigned)W;
+  };
+
+  const int gc_end = min(y0 + R, H);  // last gauss row needed
+  // Step gc produces row gc+3 = stream row gc - y0 + 6 of the pass: in-group
+  // position (gc - y0 + 1) % 5, i.e. the step's position k in the unrolled
+  // 5-step body (the body starts at gc = y0 - 1 + 5i).
+  auto step = [&](M3Row& r4, M3Row& r3, M3Row& r2, M3Row& r1, M3Row& r0, int gc, int k) {
+    gauss_thres(r4, r3, r2, r1, r0, gc);
+    if (MODE != 0 && gc > y0) median(r4, r3, r2, gc - 1);
+    if (gc < gc_end) produce(r4, k);
+  };
+
+#pragma unroll
+  for (int k = 0; k < 5; ++k) produce(s[k], k);
+  int gc = y0 - 1;
+  while (true) {
+    if (gc > gc_end) break;
+    step(s[0], s[1], s[2], s[3], s[4], gc++, 0);
+    if (gc > gc_end) break;
+    step(s[1], s[2], s[3], s[4], s[0], gc++, 1);
+    if (gc > gc_end) break;
+    step(s[2], s[3], s[4], s[0], s[1], gc++, 2);
+    if (gc > gc_end) break;
+    step(s[3], s[4], s[0], s[1], s[2], gc++, 3);
+    if (gc > gc_end) break;
+    step(s[4], s[0], s[1], s[2], s[3], gc++, 4);
+  }
+  // Bottom band (gc_end < y0 + R): rows past the frame were fetched but not
+  // consumed.  Release a partly consumed group and skip the pass's rest.
+  if (!INT) {
+    const int produced = gc_end - y0 + 6;  // rows of this pass consumed
+    int done = produced / kM3RPS;
+    if (produced % kM3RPS) {
+      st.release();
+      ++done;
+    }
+    for (; done < M3Stream<FMT, R>::GPP; ++done) {
+      st.acquire();
+      st.release();
+    }
+  }
+}
+
+template <int FMT, int R, bool INT>
+__device__ __forceinline__ void m3_walk(M3Stream<FMT, R>& st, const unsigned char* prev_tok, unsigned char* out,
+                                        unsigned char* next_tok, unsigned tmem, const MotionGeom& g, int y0, int x,
+                                        int lane, int f_begin, int f_end) {
+  const size_t frame_px = (size_t)g.W * g.H;
+  unsigned gm[2], mm[2];
+  column_masks(x, g.W, gm, mm);
+  if (f_begin == 0) {
+    // Delay token: gauss of the previous firing's last frame -> TMEM.
+    for (int r = 0; r < R + 2; ++r) {
+      unsigned a0, a1;
+      load_bytes8<true>(prev_tok, y0 - 1 + r, x, g.W, g.H, a0, a1);
+      tmem_st2(tmem + 2u * r, a0, a1);
+    }
+  } else {
+    m3_pass<FMT, R, 0, INT>(st, nullptr, nullptr, tmem, g, y0, x, lane, gm, mm);
+  }
+  const int f_last = (f_end == g.frames) ? f_end - 1 : f_end;
+  for (int f = f_begin; f < f_last; ++f)
+    m3_pass<FMT, R, 1, INT>(st, out + (size_t)f * frame_px, nullptr, tmem, g, y0, x, lane, gm, mm);
+  if (f_last < f_end)
+    m3_pass<FMT, R, 2, INT>(st, out + (size_t)f_last * frame_px, next_tok, tmem, g, y0, x, lane, gm, mm);
+}
+
+template <int FMT, int R>
+__global__ void __launch_bounds__(32 * kM3Warps, 4) motion_m3_kernel(const __grid_constant__ CUtensorMap map,
+                                                                   MotionIO io, MotionGeom g) {
+  extern __shared__ __align__(128) unsigned char m3_smem[];
+  // shfl from lane 0: the compiler then treats warp-derived values (TMEM
+  // addresses, ring addresses) as warp-uniform instead of emitting
+  // per-unique-value loops around every tcgen05.ld/st.
+  const int lane = threadIdx.x & 31, warp = __shfl_sync(0xffffffffu, (int)threadIdx.x >> 5, 0);
+  const int y0 = blockIdx.y * R;
+  const int tx0 = (int)blockIdx.x * kOutPxPerWarp - kPxPerLane;
+  const int x = tx0 + lane * kPxPerLane;
+  const int chunk = blockIdx.z * kM3Warps + warp;
+  const int f_begin = chunk * g.chunk;
+  const int f_end = min(f_begin + g.chunk, g.frames);
+
+  unsigned* tmem_slot = reinterpret_cast<unsigned*>(m3_smem + kM3Warps * m3_ring_bytes<FMT>() + kM3Warps * kM3Stages * 8);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  M3Stream<FMT, R> st;
+  st.map = &map;
+  st.ring = smem_u32(m3_smem + warp * m3_ring_bytes<FMT>());
+  st.bars = smem_u32(m3_smem + kM3Warps * m3_ring_bytes<FMT>() + warp * kM3Stages * 8);
+  st.g = 0;
+  st.stage = 0;
+  st.phase = 0;
+  st.cur = 0;
+  st.c0 = (tx0 * FMT - 8) / 4;  // 16-byte aligned box start (see m3_row_bytes)
+  st.H = g.H;
+  st.y0 = y0;
+  st.lane = lane;
+  st.fs = f_begin > 0 ? f_begin - 1 : f_begin;
+  const int passes = f_begin < f_end ? f_end - st.fs : 0;
+  st.groups = (unsigned)passes * M3Stream<FMT, R>::GPP;
+  if (lane == 0) {
+    for (int s = 0; s < kM3Stages; ++s) mbar_init(st.bars + 8 * s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const unsigned tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0) + ((unsigned)(32 * warp) << 16);
+
+  if (passes > 0) {
+    if (lane == 0)
+      for (int s = 0; s < kM3Stages; ++s) st.issue(s, s);
+    const bool interior = y0 >= 3 && y0 + R <= g.H - 3;  // no border gauss/median row
+    if (interior)
+      m3_walk<FMT, R, true>(st, io.prev, io.out, io.next, tmem, g, y0, x, lane, f_begin, f_end);
+    else
+      m3_walk<FMT, R, false>(st, io.prev, io.out, io.next, tmem, g, y0, x, lane, f_begin, f_end);
+  }
+  tmem_wait_st();
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_slot), "n"(kTmemCols) : "memory");
+  }
+}
+
+
 // Gauss of one frame given in the input format (sets a delay token from a
 // raw halo frame).
 template <int FMT>
@@ -627,6 +997,7 @@ struct df_motion {
   int cur = 0;
   unsigned* scratch = nullptr;  // done counter
   int resident_ctas = 0;        // per SM, for the temporal chunking
+  int m3_resident[3] = {0, 0, 0};  // motion_m3_kernel<R> CTAs per SM (0: M3 unavailable)
   int sms = 148;
   df::Staging staging;          // df_motion_run_host pipeline
 };
@@ -673,8 +1044,106 @@ int launch_fused(df_motion* m, const MotionIO& io, int frames, cudaStream_t s) {
   return after_launch("motion_fused_kernel");
 }
 
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+#ifndef DF_MOTION_M3
+#define DF_MOTION_M3 1
+#endif
+
+bool m3_eligible(const df_motion* m, const MotionIO& io) {
+  return DF_MOTION_M3 && !io.channel_mode && m->m3_resident[0] > 0 && ((size_t)m->W * m->fmt) % 16 == 0 &&
+         (reinterpret_cast<uintptr_t>(io.in) & 15) == 0 && tensor_map_encoder() != nullptr;
+}
+
+// Band heights M3 is built for; launch_m3 picks the one whose grid fills
+// one wave best (cost model: waves x (frames per chunk + warm-up) x rows
+// fetched per pass).
+constexpr int kM3Heights[3] = {49, 54, 59};
+
+template <int FMT>
+const void* m3_kernel_fn(int ri) {
+  return ri == 0 ? (const void*)motion_m3_kernel<FMT, kM3Heights[0]>
+                 : ri == 1 ? (const void*)motion_m3_kernel<FMT, kM3Heights[1]>
+                           : (const void*)motion_m3_kernel<FMT, kM3Heights[2]>;
+}
+
+struct M3Plan {
+  int ri, bands, chunk, chunks, slices;
+  double cost;
+};
+
+M3Plan m3_plan(const df_motion* m, int frames, int ri) {
+  const int R = kM3Heights[ri];
+  const int tiles = (m->W + kOutPxPerWarp - 1) / kOutPxPerWarp;
+  M3Plan p{};
+  p.ri = ri;
+  p.bands = (m->H + R - 1) / R;
+  const int slots = std::max(1, m->m3_resident[ri] * m->sms);  // CTAs in one wave
+  const int per_slice = tiles * p.bands;
+  // Temporal chunks (one per warp, kM3Warps per CTA): as many CTA slices as
+  // fit ONE wave (a partial second wave would double the step time).
+  p.slices = std::max(1, slots / per_slice);
+  p.chunks = std::min(p.slices * kM3Warps, frames);
+  p.chunk = (frames + p.chunks - 1) / p.chunks;
+  p.chunks = (frames + p.chunk - 1) / p.chunk;
+  const int ctas = per_slice * ((p.chunks + kM3Warps - 1) / kM3Warps);
+  const int waves = (ctas + slots - 1) / slots;
+  p.cost = (double)waves * (p.chunk + (p.chunks > 1 ? 1 : 0)) * (R + 6);
+  return p;
+}
+
+template <int FMT>
+int launch_m3(df_motion* m, const MotionIO& io, int frames, cudaStream_t s) {
+  MotionGeom g = make_geom(m, frames);
+  M3Plan best = m3_plan(m, frames, 0);
+  for (int ri = 1; ri < 3; ++ri) {
+    const M3Plan p = m3_plan(m, frames, ri);
+    if (p.cost < best.cost) best = p;
+  }
+  if (const char* force = getenv("DF_MOTION_M3_R")) {  // tests: pin the band height
+    const int ri = atoi(force);
+    if (ri >= 0 && ri < 3) best = m3_plan(m, frames, ri);
+  }
+  g.chunk = best.chunk;
+  CUtensorMap map;
+  const cuuint64_t dims[2] = {(cuuint64_t)m->W * FMT / 4, (cuuint64_t)m->H * (cuuint64_t)frames};
+  const cuuint64_t strides[1] = {(cuuint64_t)m->W * FMT};
+  const cuuint32_t box[2] = {(cuuint32_t)(m3_row_bytes<FMT>() / 4), (cuuint32_t)kM3RPS};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult cr = tensor_map_encoder()(&map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<unsigned char*>(io.in), dims,
+                                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  DF_REQUIRE(cr == CUDA_SUCCESS, DF_ECUDA, "motion: cuTensorMapEncodeTiled failed (%d)", (int)cr);
+  const int tiles = (m->W + kOutPxPerWarp - 1) / kOutPxPerWarp;
+  dim3 grid(tiles, best.bands, (best.chunks + kM3Warps - 1) / kM3Warps);
+  if (getenv("DF_DEBUG"))
+    fprintf(stderr, "motion_m3: R %d, resident %d/SM, grid %ux%ux%u, chunk %d frames, smem %zu\n",
+            kM3Heights[best.ri], m->m3_resident[best.ri], grid.x, grid.y, grid.z, g.chunk, m3_smem_bytes<FMT>());
+  const size_t smem = m3_smem_bytes<FMT>();
+  if (best.ri == 0)
+    motion_m3_kernel<FMT, kM3Heights[0]><<<grid, 32 * kM3Warps, smem, s>>>(map, io, g);
+  else if (best.ri == 1)
+    motion_m3_kernel<FMT, kM3Heights[1]><<<grid, 32 * kM3Warps, smem, s>>>(map, io, g);
+  else
+    motion_m3_kernel<FMT, kM3Heights[2]><<<grid, 32 * kM3Warps, smem, s>>>(map, io, g);
+  return after_launch("motion_m3_kernel");
+}
+
 int launch_motion(df_motion* m, const MotionIO& io, int frames, cudaStream_t s) {
   if (frames <= 0) return DF_OK;
+  if (m3_eligible(m, io))
+    return m->fmt == DF_MOTION_RGB ? launch_m3<DF_MOTION_RGB>(m, io, frames, s)
+                                   : launch_m3<DF_MOTION_GRAY>(m, io, frames, s);
   const bool fast = (m->W % 8 == 0);
   if (m->fmt == DF_MOTION_RGB)
     return fast ? launch_fused<DF_MOTION_RGB, true>(m, io, frames, s)
@@ -720,6 +1189,30 @@ int df_motion_create(int device, unsigned width, unsigned height, int fmt, uint8
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
     if (e == cudaSuccess)
       e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m->resident_ctas, fn, 32 * kWarpsPerCta, kSmemBytes);
+    if (e == cudaSuccess && DF_MOTION_M3 && ((size_t)width * fmt) % 16 == 0) {
+      const int sm3 = (int)(fmt == DF_MOTION_RGB ? m3_smem_bytes<DF_MOTION_RGB>() : m3_smem_bytes<DF_MOTION_GRAY>());
+      int smem_sm = 0;
+      e = cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
+      for (int ri = 0; ri < 3 && e == cudaSuccess; ++ri) {
+        const void* f3 = fmt == DF_MOTION_RGB ? m3_kernel_fn<DF_MOTION_RGB>(ri) : m3_kernel_fn<DF_MOTION_GRAY>(ri);
+        e = cudaFuncSetAttribute(f3, cudaFuncAttributeMaxDynamicSharedMemorySize, sm3);
+        // Residency from the kernel's resources (the occupancy API reports 1
+        // CTA/SM for kernels that allocate TMEM): TMEM (kTmemCols of 512
+        // columns per CTA), registers, shared memory (+1 KB reserved per CTA).
+        cudaFuncAttributes fa{};
+        if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, f3);
+        if (e == cudaSuccess) {
+          const int by_regs = 65536 / std::max(1, fa.numRegs * 32 * kM3Warps);
+          const int by_smem = smem_sm / (sm3 + (int)fa.sharedSizeBytes + 1024);
+          m->m3_resident[ri] = std::max(0, std::min({512 / kTmemCols, by_regs, by_smem}));
+        }
+      }
+      if (e != cudaSuccess || m->m3_resident[0] == 0 || m->m3_resident[1] == 0 || m->m3_resident[2] == 0) {
+        m->m3_resident[0] = 0;  // M3 unavailable: the register-prefetch kernel runs
+        e = cudaSuccess;
+        cudaGetLastError();
+      }
+    }
   }
   if (e != cudaSuccess) {
     int rc = cuda_status(e, "df_motion_create");

@@ -102,6 +102,18 @@ def test_interior_bands_temporal_chunks_structured(gpu):
         assert_frames_equal(run_gpu(frames.reshape(-1), w, h, 40, chunk=chunk), want, w, h)
 
 
+@pytest.mark.parametrize("ri", [0, 1, 2])
+@pytest.mark.parametrize("w,h,fmt,n,chunk", [(1280, 300, 3, 9, 4), (320, 240, 1, 13, 0), (640, 137, 3, 5, 1),
+                                             (96, 40, 3, 6, 2)])
+def test_tma_tmem_band_heights(gpu, monkeypatch, ri, w, h, fmt, n, chunk):
+    # The TMA/TMEM kernel (rows 16-byte aligned: W*FMT % 16 == 0) at each of
+    # its band heights, across firings (delay token) and temporal chunks.
+    monkeypatch.setenv("DF_MOTION_M3_R", str(ri))
+    f = O.synth_bytes(n * w * h * fmt, 100 * ri + w + h)
+    want = O.motion_rgb(f, w, h) if fmt == 3 else O.motion_gray(f, w, h)
+    assert_frames_equal(run_gpu(f, w, h, fmt=fmt, chunk=chunk), want, w, h)
+
+
 def test_many_frames_temporal_chunks(gpu):
     # Enough frames that the kernel splits the firing into frame ranges,
     # each recomputing gauss(f0 - 1) on chip.

@@ -27,9 +27,21 @@ def show(name, got, want, w, h):
     print("   row", r, "want", wv[r, :24].tolist())
 
 
-for (w, h, n, fmt) in [(96, 40, 6, 1), (96, 40, 6, 3), (96, 40, 1, 1), (96, 8, 1, 1), (64, 48, 2, 1),
-                       (16, 8, 1, 1), (16, 8, 2, 1), (320, 240, 64, 1)]:
-    src = O.synth_bytes(n * w * h * fmt, 606)
-    got = motion.run(src, w, h, 32, fmt)
-    want = O.motion_rgb(src, w, h) if fmt == 3 else O.motion_gray(src, w, h)
-    show(f"{w}x{h}x{n} fmt{fmt}", got, want, w, h)
+CASES = [(96, 40, 6, 1), (96, 40, 6, 3), (96, 40, 1, 1), (96, 8, 1, 1), (64, 48, 2, 1),
+         (16, 8, 1, 1), (16, 8, 2, 1), (320, 240, 64, 1)]
+if len(sys.argv) > 1:
+    CASES = [tuple(int(v) for v in a.split(",")) for a in sys.argv[1:]]
+def _main():
+  for case in CASES:
+      w, h, n, fmt = case[:4]
+      chunk = case[4] if len(case) > 4 else 0
+      src = O.synth_bytes(n * w * h * fmt, 606)
+      a = motion.MotionActor(w, h, fmt, 32)
+      got = np.empty(n * w * h, np.uint8)
+      a.run_host(src, got, chunk_frames=chunk)
+      want = O.motion_rgb(src, w, h) if fmt == 3 else O.motion_gray(src, w, h)
+      show(f"{w}x{h}x{n} fmt{fmt} chunk{chunk}", got, want, w, h)
+
+
+if __name__ == '__main__':
+    _main()
