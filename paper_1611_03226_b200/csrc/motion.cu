@@ -718,7 +718,8 @@ struct M3Row {
 // warp's (tile, band).  INT: interior band (no border rows, full R rows).
 template <int FMT, int R, int MODE, bool INT>
 __device__ __forceinline__ void m3_pass(M3Stream<FMT, R>& st, unsigned char* __restrict__ out,
-                                        unsigned char* __restrict__ next_tok, unsigned tmem, const MotionGeom& g,
+                                        unsigned char* __restrict__ next_tok, unsigned char* __restrict__ next_copy,
+                                        unsigned tmem, const MotionGeom& g,
                                         int y0, int x, int lane, const unsigned gm[2], const unsigned mm[2]) {
   const int W = g.W, H = g.H;
   const bool out_lane = lane >= 1 && lane <= 30;
@@ -776,8 +777,11 @@ __device__ __forceinline__ void m3_pass(M3Stream<FMT, R>& st, unsigned char* __r
       r2.t[1] = thres4(gw[1], p1, g);
     }
     tmem_st2(ta, gw[0], gw[1]);
-    if (MODE == 2 && out_lane && x < W && gc >= y0 && gc < y0 + R && gc < H)
-      *reinterpret_cast<uint2*>(next_tok + ((unsigned)gc * (unsigned)W + (unsigned)x)) = make_uint2(gw[0], gw[1]);
+    if (MODE == 2 && out_lane && x < W && gc >= y0 && gc < y0 + R && gc < H) {
+      const unsigned o = (unsigned)gc * (unsigned)W + (unsigned)x;
+      *reinterpret_cast<uint2*>(next_tok + o) = make_uint2(gw[0], gw[1]);
+      if (next_copy) *reinterpret_cast<uint2*>(next_copy + o) = make_uint2(gw[0], gw[1]);  // Fig. 2 phase 2
+    }
   };
 
   auto median = [&](M3Row& r4, M3Row& r3, M3Row& r2, int m) {
@@ -842,7 +846,7 @@ __device__ __forceinline__ void m3_pass(M3Stream<FMT, R>& st, unsigned char* __r
 
 template <int FMT, int R, bool INT>
 __device__ __forceinline__ void m3_walk(M3Stream<FMT, R>& st, const unsigned char* prev_tok, unsigned char* out,
-                                        unsigned char* next_tok, unsigned tmem, const MotionGeom& g, int y0, int x,
+                                        unsigned char* next_tok, unsigned char* next_copy, unsigned tmem, const MotionGeom& g, int y0, int x,
                                         int lane, int f_begin, int f_end) {
   const size_t frame_px = (size_t)g.W * g.H;
   unsigned gm[2], mm[2];
@@ -855,18 +859,19 @@ __device__ __forceinline__ void m3_walk(M3Stream<FMT, R>& st, const unsigned cha
       tmem_st2(tmem + 2u * r, a0, a1);
     }
   } else {
-    m3_pass<FMT, R, 0, INT>(st, nullptr, nullptr, tmem, g, y0, x, lane, gm, mm);
+    m3_pass<FMT, R, 0, INT>(st, nullptr, nullptr, nullptr, tmem, g, y0, x, lane, gm, mm);
   }
   const int f_last = (f_end == g.frames) ? f_end - 1 : f_end;
   for (int f = f_begin; f < f_last; ++f)
-    m3_pass<FMT, R, 1, INT>(st, out + (size_t)f * frame_px, nullptr, tmem, g, y0, x, lane, gm, mm);
+    m3_pass<FMT, R, 1, INT>(st, out + (size_t)f * frame_px, nullptr, nullptr, tmem, g, y0, x, lane, gm, mm);
   if (f_last < f_end)
-    m3_pass<FMT, R, 2, INT>(st, out + (size_t)f_last * frame_px, next_tok, tmem, g, y0, x, lane, gm, mm);
+    m3_pass<FMT, R, 2, INT>(st, out + (size_t)f_last * frame_px, next_tok, next_copy, tmem, g, y0, x, lane, gm, mm);
 }
 
 template <int FMT, int R>
 __global__ void __launch_bounds__(32 * kM3Warps, 4) motion_m3_kernel(const __grid_constant__ CUtensorMap map,
-                                                                   MotionIO io, MotionGeom g) {
+                                                                   MotionIO io, MotionGeom g,
+                                                                   unsigned* done_counter) {
   extern __shared__ __align__(128) unsigned char m3_smem[];
   // shfl from lane 0: the compiler then treats warp-derived values (TMEM
   // addresses, ring addresses) as warp-uniform instead of emitting
@@ -897,9 +902,25 @@ __global__ void __launch_bounds__(32 * kM3Warps, 4) motion_m3_kernel(const __gri
   st.c0 = (tx0 * FMT - 8) / 4;  // 16-byte aligned box start (see m3_row_bytes)
   st.H = g.H;
   st.y0 = y0;
+  // Channel mode: the map covers the input channel's whole storage; the
+  // firing's region (resolved from the device phase) starts at frame slot
+  // `base` of it.  Raw mode: the map covers exactly the firing's frames.
+  unsigned char* out = io.out;
+  const unsigned char* prev_tok = io.prev;
+  unsigned char* next_tok = io.next;
+  unsigned char* next_copy = io.next_copy;
+  int base = 0;
+  if (io.channel_mode) {
+    base = (int)((size_t)(chan_read_region(io.in_ch) - io.in_ch.storage) / io.in_ch.token_size);
+    out = chan_write_region(io.out_ch);
+    prev_tok = chan_read_region(io.delay_ch);
+    next_tok = chan_write_region(io.delay_ch);
+    next_copy = chan_write_wraps(io.delay_ch) ? io.delay_ch.storage : nullptr;
+  }
   st.lane = lane;
-  st.fs = f_begin > 0 ? f_begin - 1 : f_begin;
-  const int passes = f_begin < f_end ? f_end - st.fs : 0;
+  const int f_first = f_begin > 0 ? f_begin - 1 : f_begin;  // warm-up frame of a later chunk
+  st.fs = base + f_first;
+  const int passes = f_begin < f_end ? f_end - f_first : 0;
   st.groups = (unsigned)passes * M3Stream<FMT, R>::GPP;
   if (lane == 0) {
     for (int s = 0; s < kM3Stages; ++s) mbar_init(st.bars + 8 * s, 1);
@@ -915,9 +936,9 @@ __global__ void __launch_bounds__(32 * kM3Warps, 4) motion_m3_kernel(const __gri
       for (int s = 0; s < kM3Stages; ++s) st.issue(s, s);
     const bool interior = y0 >= 3 && y0 + R <= g.H - 3;  // no border gauss/median row
     if (interior)
-      m3_walk<FMT, R, true>(st, io.prev, io.out, io.next, tmem, g, y0, x, lane, f_begin, f_end);
+      m3_walk<FMT, R, true>(st, prev_tok, out, next_tok, next_copy, tmem, g, y0, x, lane, f_begin, f_end);
     else
-      m3_walk<FMT, R, false>(st, io.prev, io.out, io.next, tmem, g, y0, x, lane, f_begin, f_end);
+      m3_walk<FMT, R, false>(st, prev_tok, out, next_tok, next_copy, tmem, g, y0, x, lane, f_begin, f_end);
   }
   tmem_wait_st();
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -925,6 +946,22 @@ __global__ void __launch_bounds__(32 * kM3Warps, 4) motion_m3_kernel(const __gri
   if (warp == 0) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_slot), "n"(kTmemCols) : "memory");
+  }
+  if (io.channel_mode) {  // the last CTA commits the firing (as motion_fused_kernel)
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+      __threadfence();
+      last = atomicAdd(done_counter, 1u) == gridDim.x * gridDim.y * gridDim.z - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+      __threadfence();
+      *done_counter = 0;
+      chan_commit_read(io.in_ch, io.in_ch.rate);
+      chan_commit_read(io.delay_ch, 1);
+      chan_commit_write(io.delay_ch, 1);
+      chan_commit_write(io.out_ch, io.out_ch.rate);
+    }
   }
 }
 
@@ -1061,8 +1098,9 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 #endif
 
 bool m3_eligible(const df_motion* m, const MotionIO& io) {
-  return DF_MOTION_M3 && !io.channel_mode && m->m3_resident[0] > 0 && ((size_t)m->W * m->fmt) % 16 == 0 &&
-         (reinterpret_cast<uintptr_t>(io.in) & 15) == 0 && tensor_map_encoder() != nullptr;
+  const void* base = io.channel_mode ? (const void*)io.in_ch.storage : (const void*)io.in;
+  return DF_MOTION_M3 && m->m3_resident[0] > 0 && ((size_t)m->W * m->fmt) % 16 == 0 &&
+         (reinterpret_cast<uintptr_t>(base) & 15) == 0 && tensor_map_encoder() != nullptr;
 }
 
 // Band heights M3 is built for; launch_m3 picks the one whose grid fills
@@ -1115,12 +1153,17 @@ int launch_m3(df_motion* m, const MotionIO& io, int frames, cudaStream_t s) {
     if (ri >= 0 && ri < 3) best = m3_plan(m, frames, ri);
   }
   g.chunk = best.chunk;
+  // Raw mode: the map covers the firing's frames; channel mode: the input
+  // channel's whole storage (the kernel offsets to its region).
+  const void* base = io.channel_mode ? (const void*)io.in_ch.storage : (const void*)io.in;
+  const unsigned long long map_frames =
+      io.channel_mode ? chan_capacity_tokens(io.in_ch.rate, io.in_ch.has_delay) : (unsigned long long)frames;
   CUtensorMap map;
-  const cuuint64_t dims[2] = {(cuuint64_t)m->W * FMT / 4, (cuuint64_t)m->H * (cuuint64_t)frames};
+  const cuuint64_t dims[2] = {(cuuint64_t)m->W * FMT / 4, (cuuint64_t)m->H * (cuuint64_t)map_frames};
   const cuuint64_t strides[1] = {(cuuint64_t)m->W * FMT};
   const cuuint32_t box[2] = {(cuuint32_t)(m3_row_bytes<FMT>() / 4), (cuuint32_t)kM3RPS};
   const cuuint32_t estr[2] = {1, 1};
-  CUresult cr = tensor_map_encoder()(&map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<unsigned char*>(io.in), dims,
+  CUresult cr = tensor_map_encoder()(&map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void*>(base), dims,
                                      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   DF_REQUIRE(cr == CUDA_SUCCESS, DF_ECUDA, "motion: cuTensorMapEncodeTiled failed (%d)", (int)cr);
@@ -1131,11 +1174,11 @@ int launch_m3(df_motion* m, const MotionIO& io, int frames, cudaStream_t s) {
             kM3Heights[best.ri], m->m3_resident[best.ri], grid.x, grid.y, grid.z, g.chunk, m3_smem_bytes<FMT>());
   const size_t smem = m3_smem_bytes<FMT>();
   if (best.ri == 0)
-    motion_m3_kernel<FMT, kM3Heights[0]><<<grid, 32 * kM3Warps, smem, s>>>(map, io, g);
+    motion_m3_kernel<FMT, kM3Heights[0]><<<grid, 32 * kM3Warps, smem, s>>>(map, io, g, m->scratch);
   else if (best.ri == 1)
-    motion_m3_kernel<FMT, kM3Heights[1]><<<grid, 32 * kM3Warps, smem, s>>>(map, io, g);
+    motion_m3_kernel<FMT, kM3Heights[1]><<<grid, 32 * kM3Warps, smem, s>>>(map, io, g, m->scratch);
   else
-    motion_m3_kernel<FMT, kM3Heights[2]><<<grid, 32 * kM3Warps, smem, s>>>(map, io, g);
+    motion_m3_kernel<FMT, kM3Heights[2]><<<grid, 32 * kM3Warps, smem, s>>>(map, io, g, m->scratch);
   return after_launch("motion_m3_kernel");
 }
 

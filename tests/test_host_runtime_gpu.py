@@ -51,6 +51,18 @@ def test_motion_network_equals_oracle(gpu, rate, fmt):
     assert delay_written == n // rate  # one delay token per firing through the self-loop
 
 
+@pytest.mark.parametrize("w,h,fmt,rate", [(640, 200, 3, 3), (1280, 136, 1, 5)])
+def test_motion_network_large_frames(gpu, w, h, fmt, rate):
+    # Frames with interior bands and several tiles: the TMA/TMEM kernel in
+    # channel mode (region and delay token resolved from device phases).
+    n = 4 * rate
+    f = O.synth_bytes(n * w * h * fmt, w + h + rate)
+    got, _, delay_written = H.motion_run(f, w, h, fmt, 32, rate)
+    want = O.motion_rgb(f, w, h) if fmt == 3 else O.motion_gray(f, w, h)
+    np.testing.assert_array_equal(got, want)
+    assert delay_written == n // rate
+
+
 def test_motion_acceptance6_through_runtime(gpu, hashes):
     import hashlib
     h = hashes["motion_acceptance6"]
