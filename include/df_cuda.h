@@ -234,6 +234,11 @@ int df_motion_fire_channels(df_motion* m, df_channel* in, df_channel* delay, df_
  * current delay token.  Synchronizes before returning. */
 int df_motion_run_host(df_motion* m, const void* in_host, uint8_t* out_host, uint64_t frames,
                        uint32_t chunk_frames, void* stream);
+/* Name of the kernel a firing of this actor launches when its input is
+ * 16-byte aligned: "motion_m3_kernel" (TMA-fed rows, TMEM-resident delay
+ * band; needs width * input_format % 16 == 0) or "motion_fused_kernel"
+ * (register-prefetch kernel, any width).  Static storage. */
+const char* df_motion_kernel_name(const df_motion* m);
 /* Individual stages (unit-level parity with gauss5x5 / thres_diff /
  * median5 / rgb->gray); one frame each, device buffers. */
 int df_motion_gauss5x5(const uint8_t* in_dev, uint8_t* out_dev, unsigned w, unsigned h,

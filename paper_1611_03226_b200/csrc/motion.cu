@@ -1361,6 +1361,13 @@ int df_motion_run_host(df_motion* m, const void* in_host, uint8_t* out_host, uin
       [&](uint64_t c, unsigned char* din, unsigned char* dout) { return df_motion_fire(m, din, dout, nf(c), cs); });
 }
 
+const char* df_motion_kernel_name(const df_motion* m) {
+  if (!m) return "";
+  return DF_MOTION_M3 && m->m3_resident[0] > 0 && ((size_t)m->W * m->fmt) % 16 == 0 && tensor_map_encoder()
+             ? "motion_m3_kernel"
+             : "motion_fused_kernel";
+}
+
 int df_motion_gauss5x5(const uint8_t* in_dev, uint8_t* out_dev, unsigned w, unsigned h, void* stream) {
   DF_REQUIRE(in_dev && out_dev, DF_EINVAL, "gauss5x5: null buffer");
   DF_REQUIRE(w >= 5 && h >= 5, DF_EINVAL, "gauss5x5: frame smaller than the 5x5 kernel");

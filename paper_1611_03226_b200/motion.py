@@ -39,6 +39,11 @@ class MotionActor:
         call("df_motion_fire", self.handle, inp.at(in_offset), out.at(out_offset), int(frames),
              stream.handle if stream else None)
 
+    @property
+    def kernel_name(self) -> str:
+        """The kernel a firing launches (for 16-byte aligned inputs)."""
+        return lib().df_motion_kernel_name(self.handle).decode()
+
     def fire_channels(self, in_ch, delay_ch, out_ch, stream: Stream | None = None):
         call("df_motion_fire_channels", self.handle, in_ch.handle, delay_ch.handle, out_ch.handle,
              stream.handle if stream else None)
