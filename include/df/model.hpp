@@ -14,6 +14,7 @@
 #include <cstdint>
 #include <functional>
 #include <optional>
+#include <span>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -79,14 +80,56 @@ class FiringContext {
   std::uint64_t firing_index_ = 0;
 };
 
-// model.hpp:103-108: mandatory fire; optional init / finish.  A dynamic
-// GPU actor sets device_control: its kernels consume one control token per
-// logical firing on the device (rates 0 or r decided there).
+// Per-firing view handed to a CPU (host) actor: the reference's
+// FiringContext (model.hpp:43-83) -- byte spans over the firing's input and
+// output regions, regular ports in declaration order, tokens per port and
+// the firing index.  The spans are pinned host copies: the runtime moves the
+// input regions device -> host before the firing and the output regions
+// host -> device after it, in the actor's stream order, so CPU and GPU
+// actors share the same device channels (the paper's heterogeneous
+// mapping).
+class HostFiringContext {
+ public:
+  std::size_t input_count() const { return inputs_.size(); }
+  std::size_t output_count() const { return outputs_.size(); }
+  std::span<const std::byte> input(std::size_t i) const { return inputs_.at(i); }
+  std::span<std::byte> output(std::size_t i) const { return outputs_.at(i); }
+  std::size_t input_tokens(std::size_t i) const { return in_tokens_.at(i); }
+  std::size_t output_tokens(std::size_t i) const { return out_tokens_.at(i); }
+  std::size_t input_token_size(std::size_t i) const { return inputs_.at(i).size() / in_tokens_.at(i); }
+  std::size_t output_token_size(std::size_t i) const { return outputs_.at(i).size() / out_tokens_.at(i); }
+  std::uint64_t firing_index() const { return firing_index_; }
+
+  // Assembled by the runtime.
+  void bind(std::vector<std::span<const std::byte>> in, std::vector<std::size_t> in_tokens,
+            std::vector<std::span<std::byte>> out, std::vector<std::size_t> out_tokens, std::uint64_t firing) {
+    inputs_ = std::move(in);
+    in_tokens_ = std::move(in_tokens);
+    outputs_ = std::move(out);
+    out_tokens_ = std::move(out_tokens);
+    firing_index_ = firing;
+  }
+
+ private:
+  std::vector<std::span<const std::byte>> inputs_;
+  std::vector<std::span<std::byte>> outputs_;
+  std::vector<std::size_t> in_tokens_, out_tokens_;
+  std::uint64_t firing_index_ = 0;
+};
+
+// model.hpp:103-108: mandatory fire; optional init / finish.  A GPU actor
+// sets `fire` (it enqueues device work); a CPU actor sets `host_fire`
+// instead (it computes on host spans, in stream order -- static rates
+// only).  A dynamic GPU actor sets device_control: its kernels consume one
+// control token per logical firing on the device (rates 0 or r decided
+// there).
 struct ActorBehavior {
   std::function<void(FiringContext&)> fire;
+  std::function<void(HostFiringContext&)> host_fire;
   std::function<void()> init;
   std::function<void()> finish;
   bool device_control = false;
+  bool is_host() const { return static_cast<bool>(host_fire); }
 };
 
 struct ActorSpec {

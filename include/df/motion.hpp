@@ -30,4 +30,17 @@ struct Params {
 NetworkGraph build_network(const Params& params);
 std::uint64_t source_firings(const Params& params);
 
+// Heterogeneous network (CPU + GPU actors on shared device channels, the
+// paper's mixed mapping): source (H2D, RGB) -> gray (CPU actor: BT.601
+// integer luma) -> motion (GPU actor, gray input) -> census (CPU actor:
+// counts moving pixels per frame into `counts`, passes the masks on) ->
+// sink (D2H).  census throws at firing `fail_at_firing` when >= 0 (fault
+// injection: the run ends in ActorFault("census")).
+struct MixedParams {
+  Params base;                       // input_format must be rgb
+  std::span<std::uint32_t> counts;   // frames entries (host)
+  std::int64_t fail_at_firing = -1;
+};
+NetworkGraph build_mixed_network(const MixedParams& params);
+
 }  // namespace df::motion

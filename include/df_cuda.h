@@ -68,6 +68,10 @@ int df_memcpy_h2d(void* dst, const void* src, size_t bytes, void* stream);
 int df_memcpy_d2h(void* dst, const void* src, size_t bytes, void* stream);
 int df_memcpy_d2d(void* dst, const void* src, size_t bytes, void* stream);
 int df_memset(void* dst, int value, size_t bytes, void* stream);
+/* Runs fn(user) on a host thread in `stream` order (cudaLaunchHostFunc):
+ * the firing of a CPU actor between its inputs' D2H and outputs' H2D.
+ * fn must not call CUDA. */
+int df_launch_host_func(void* stream, void (*fn)(void*), void* user);
 
 /* ---- device channels (Eq. 1 capacity, Fig. 2 slot walk, state in HBM) ---
  * Replaces Channel (include/dynflow/channel.hpp:71-135).  Storage is

@@ -34,10 +34,19 @@ int dfh_motion_run(int device, const uint8_t* in_host, uint8_t* out_host, uint64
                    unsigned height, int input_format, uint8_t threshold, uint32_t token_rate,
                    double* sink_active_ms, uint64_t* delay_tokens_written);
 
+/* Heterogeneous CPU + GPU network (df::motion::build_mixed_network):
+ * RGB in; the gray conversion and a per-frame moving-pixel census run as
+ * CPU actors, the motion chain as a GPU actor, all on device channels.
+ * counts: `frames` entries.  fail_at_firing >= 0 injects a fault into the
+ * census actor (the call then fails with ActorFault). */
+int dfh_motion_run_mixed(int device, const uint8_t* rgb_host, uint8_t* out_host, uint64_t frames, unsigned width,
+                         unsigned height, uint8_t threshold, uint32_t token_rate, uint32_t* counts,
+                         int64_t fail_at_firing, double* sink_active_ms);
+
 /* Host-side rule checks (no device): builds the named reference network
  * shape and returns the number of validate() violations (0 = runnable);
  * -1 with dfh_last_error() on a BuildError / invalid_argument. */
-int dfh_validate_demo(int which);
+int dfh_validate_demo(int which);  /* which: 0..4, see host_abi.cpp */
 
 #ifdef __cplusplus
 }

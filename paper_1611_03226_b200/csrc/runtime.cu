@@ -145,6 +145,12 @@ int df_free(void* dptr) {
   DF_CHECK_CUDA(cudaFree(dptr));
   return DF_OK;
 }
+int df_launch_host_func(void* stream, void (*fn)(void*), void* user) {
+  DF_REQUIRE(fn, DF_EINVAL, "df_launch_host_func: null function");
+  DF_CHECK_CUDA(cudaLaunchHostFunc(as_stream(stream), fn, user));
+  return DF_OK;
+}
+
 int df_host_alloc(size_t bytes, void** hptr) {
   DF_REQUIRE(hptr, DF_EINVAL, "df_host_alloc: null out pointer");
   DF_CHECK_CUDA(cudaHostAlloc(hptr, bytes ? bytes : 1, cudaHostAllocPortable));

@@ -95,6 +95,32 @@ int dfh_motion_run(int device, const uint8_t* in_host, uint8_t* out_host, uint64
   });
 }
 
+int dfh_motion_run_mixed(int device, const uint8_t* rgb_host, uint8_t* out_host, uint64_t frames, unsigned width,
+                         unsigned height, uint8_t threshold, uint32_t rate, uint32_t* counts,
+                         int64_t fail_at_firing, double* sink_active_ms) {
+  return guarded([&] {
+    df::motion::MixedParams mp;
+    df::motion::Params& p = mp.base;
+    p.width = width;
+    p.height = height;
+    p.threshold = threshold;
+    p.token_rate = rate;
+    p.frames = frames;
+    p.input_format = df::motion::Input::rgb;
+    const std::size_t px = std::size_t(width) * height;
+    p.input = {rgb_host, frames * px * 3};
+    p.output = {out_host, frames * px};
+    mp.counts = {counts, frames};
+    mp.fail_at_firing = fail_at_firing;
+    df::NetworkGraph net = df::motion::build_mixed_network(mp);
+    df::ExecutionConfig cfg;
+    cfg.device = device;
+    cfg.source_firing_limit = df::motion::source_firings(p);
+    df::RunStats st = df::run(net, cfg);
+    if (sink_active_ms) *sink_active_ms = st.actor("sink").active_ms;
+  });
+}
+
 int dfh_validate_demo(int which) {
   int n = -1;
   int rc = guarded([&] {
@@ -140,6 +166,29 @@ int dfh_validate_demo(int which) {
                         {{PortDirection::input, PortKind::regular, "loop"},
                          {PortDirection::output, PortKind::regular, "loop"}},
                         b});
+      n = (int)validate(build_network(actors, chans)).size();
+      return;
+    }
+    if (which == 4) {  // CPU actor rules: dynamic host actor, host + device fire on one actor
+      chans = {{"c", 4, 1, false, {}}, {"d", 4, 1, false, {}}, {"e", 4, 1, false, {}}};
+      ActorBehavior src;
+      src.fire = noop;
+      actors.push_back({"src", ActorKind::static_rate,
+                        {{PortDirection::output, PortKind::regular, "c"},
+                         {PortDirection::output, PortKind::regular, "d"}},
+                        src});
+      ActorBehavior dyn;
+      dyn.host_fire = [](HostFiringContext&) {};
+      dyn.device_control = true;
+      actors.push_back({"dyn", ActorKind::dynamic_rate,
+                        {{PortDirection::input, PortKind::control, "c"},
+                         {PortDirection::input, PortKind::regular, "d"},
+                         {PortDirection::output, PortKind::regular, "e"}},
+                        dyn});
+      ActorBehavior both;
+      both.fire = noop;
+      both.host_fire = [](HostFiringContext&) {};
+      actors.push_back({"both", ActorKind::static_rate, {{PortDirection::input, PortKind::regular, "e"}}, both});
       n = (int)validate(build_network(actors, chans)).size();
       return;
     }

@@ -9,9 +9,12 @@
 #include "df/runtime.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstring>
+#include <deque>
 #include <functional>
+#include <mutex>
 #include <sstream>
 
 #include "df_cuda.h"
@@ -56,7 +59,74 @@ struct ActorRun {
   std::vector<Dep> deps;
   FiringContext ctx;
   std::uint64_t firings = 0;
+  // CPU actors: pinned host copies of the firing's regions, one per
+  // regular port (token_size * rate bytes).  Firings of one actor are
+  // serialised on its stream, so one copy per port suffices.
+  std::vector<std::byte*> stage_in, stage_out;
+  std::vector<std::size_t> bytes_in, bytes_out, tokens_in, tokens_out;
 };
+
+// Fault raised inside a CPU actor's host_fire (which runs on a CUDA
+// callback thread): recorded once, rethrown as ActorFault after the run;
+// later host firings are skipped (the reference aborts the run,
+// runtime.cpp:232-247).
+struct HostFaults {
+  std::atomic<bool> failed{false};
+  std::mutex mu;
+  std::string actor, what;
+};
+
+struct HostJob {
+  HostFaults* faults;
+  const ActorRun* run;
+  std::uint64_t firing;
+};
+
+void host_job_entry(void* p) {
+  const HostJob& job = *static_cast<const HostJob*>(p);
+  if (job.faults->failed.load()) return;
+  const ActorRun& r = *job.run;
+  try {
+    std::vector<std::span<const std::byte>> in;
+    std::vector<std::span<std::byte>> out;
+    for (std::size_t k = 0; k < r.stage_in.size(); ++k) in.emplace_back(r.stage_in[k], r.bytes_in[k]);
+    for (std::size_t k = 0; k < r.stage_out.size(); ++k) out.emplace_back(r.stage_out[k], r.bytes_out[k]);
+    HostFiringContext ctx;
+    ctx.bind(std::move(in), r.tokens_in, std::move(out), r.tokens_out, job.firing);
+    r.spec->behavior.host_fire(ctx);
+  } catch (const std::exception& e) {
+    std::lock_guard<std::mutex> lock(job.faults->mu);
+    if (!job.faults->failed.exchange(true)) {
+      job.faults->actor = r.spec->id;
+      job.faults->what = e.what();
+    }
+  } catch (...) {
+    std::lock_guard<std::mutex> lock(job.faults->mu);
+    if (!job.faults->failed.exchange(true)) {
+      job.faults->actor = r.spec->id;
+      job.faults->what = "unknown exception";
+    }
+  }
+}
+
+// One firing of a CPU actor, all in its stream: inputs' regions D2H, the
+// host function, outputs' regions H2D, then the channel commits.
+void fire_host_actor(ActorRun& r, std::uint64_t firing, HostFaults& faults, std::deque<HostJob>& jobs) {
+  const std::size_t nin = r.ctx.input_count(), nout = r.ctx.output_count();
+  std::vector<df_region> rin(nin), rout(nout);
+  for (std::size_t k = 0; k < nin; ++k) {
+    check(df_channel_read_start(r.ctx.input(k), r.tokens_in[k], &rin[k]));
+    check(df_memcpy_d2h(r.stage_in[k], rin[k].dptr, r.bytes_in[k], r.stream));
+  }
+  for (std::size_t k = 0; k < nout; ++k) check(df_channel_write_start(r.ctx.output(k), r.tokens_out[k], &rout[k]));
+  jobs.push_back({&faults, &r, firing});
+  check(df_launch_host_func(r.stream, host_job_entry, &jobs.back()));
+  for (std::size_t k = 0; k < nout; ++k) {
+    check(df_memcpy_h2d(rout[k].dptr, r.stage_out[k], r.bytes_out[k], r.stream));
+    check(df_channel_write_end(r.ctx.output(k), &rout[k], r.stream));
+  }
+  for (std::size_t k = 0; k < nin; ++k) check(df_channel_read_end(r.ctx.input(k), &rin[k], r.stream));
+}
 
 // Topological order over undelayed channels (validate() rejected cycles).
 std::vector<std::size_t> topo_order(const NetworkGraph& net) {
@@ -101,6 +171,9 @@ RunStats run(const NetworkGraph& net, const ExecutionConfig& cfg) {
   std::vector<ActorRun> runs(net.actors().size());
   auto cleanup = [&]() {
     for (ActorRun& r : runs) {
+      if (r.stream) df_stream_synchronize(r.stream);  // host callbacks may still reference the stages
+      for (std::byte* b : r.stage_in) df_host_free(b);
+      for (std::byte* b : r.stage_out) df_host_free(b);
       for (void*& e : r.done)
         if (e) df_event_destroy(e);
       if (r.t_first) df_event_destroy(r.t_first);
@@ -136,6 +209,19 @@ RunStats run(const NetworkGraph& net, const ExecutionConfig& cfg) {
         else
           out.push_back(chans[c]);
       }
+      if (r.spec->behavior.is_host()) {
+        auto stage = [&](df_channel* ch, std::vector<std::byte*>& bufs, std::vector<std::size_t>& bytes,
+                         std::vector<std::size_t>& tokens) {
+          const std::size_t n = df_channel_token_rate(ch), b = n * df_channel_token_size(ch);
+          void* h = nullptr;
+          check(df_host_alloc(b, &h));
+          bufs.push_back(static_cast<std::byte*>(h));
+          bytes.push_back(b);
+          tokens.push_back(n);
+        };
+        for (df_channel* ch : in) stage(ch, r.stage_in, r.bytes_in, r.tokens_in);
+        for (df_channel* ch : out) stage(ch, r.stage_out, r.bytes_out, r.tokens_out);
+      }
       r.ctx.bind(std::move(in), std::move(out), ctrl);
     }
     // Dependencies encoding the channel protocol (see df/runtime.hpp).
@@ -157,6 +243,8 @@ RunStats run(const NetworkGraph& net, const ExecutionConfig& cfg) {
   const std::vector<std::size_t> order = topo_order(net);
   const std::uint64_t limit = cfg.source_firing_limit.value_or(0);
   std::string fault_actor;
+  HostFaults host_faults;
+  std::deque<HostJob> host_jobs;  // alive until every stream has drained
   try {
     for (ActorRun& r : runs) {
       fault_actor = r.spec->id;
@@ -173,7 +261,10 @@ RunStats run(const NetworkGraph& net, const ExecutionConfig& cfg) {
         if (i == 0) check(df_event_record(r.t_first, r.stream));
         r.ctx.reset(i, r.stream, cfg.device);
         fault_actor = r.spec->id;
-        r.spec->behavior.fire(r.ctx);
+        if (r.spec->behavior.is_host())
+          fire_host_actor(r, i, host_faults, host_jobs);
+        else
+          r.spec->behavior.fire(r.ctx);
         fault_actor.clear();
         check(df_event_record(r.done[i % 3], r.stream));
         ++r.firings;
@@ -182,6 +273,10 @@ RunStats run(const NetworkGraph& net, const ExecutionConfig& cfg) {
     for (ActorRun& r : runs) {
       check(df_event_record(r.t_last, r.stream));
       check(df_stream_synchronize(r.stream));
+    }
+    if (host_faults.failed.load()) {
+      fault_actor = host_faults.actor;
+      throw std::runtime_error(host_faults.what);
     }
     for (ActorRun& r : runs) {
       fault_actor = r.spec->id;

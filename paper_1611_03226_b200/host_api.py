@@ -30,6 +30,8 @@ def lib():
                                   C.POINTER(C.c_uint64)]
         L.dfh_motion_run.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint, C.c_uint, C.c_int,
                                      C.c_uint8, C.c_uint32, C.POINTER(C.c_double), C.POINTER(C.c_uint64)]
+        L.dfh_motion_run_mixed.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint, C.c_uint,
+                                           C.c_uint8, C.c_uint32, C.c_void_p, C.c_int64, C.POINTER(C.c_double)]
         L.dfh_validate_demo.argtypes = [C.c_int]
         _h = L
     return _h
@@ -65,6 +67,21 @@ def motion_run(frames: np.ndarray, width: int, height: int, fmt: int = 1, thresh
     _check(lib().dfh_motion_run(device, frames.ctypes.data_as(C.c_void_p), out.ctypes.data_as(C.c_void_p), n, width,
                                 height, fmt, threshold, rate, C.byref(ms), C.byref(dw)))
     return out, ms.value, dw.value
+
+
+def motion_run_mixed(rgb: np.ndarray, width: int, height: int, threshold: int = 32, rate: int = 1,
+                     device: int = 0, fail_at_firing: int = -1):
+    """run(motion::build_mixed_network(params)): CPU gray + census actors around the
+    GPU motion actor; returns (masks, per-frame moving-pixel counts, sink_active_ms)."""
+    rgb = np.ascontiguousarray(rgb, np.uint8).reshape(-1)
+    n = rgb.size // (width * height * 3)
+    out = np.empty(n * width * height, np.uint8)
+    counts = np.zeros(n, np.uint32)
+    ms = C.c_double(0)
+    _check(lib().dfh_motion_run_mixed(device, rgb.ctypes.data_as(C.c_void_p), out.ctypes.data_as(C.c_void_p), n,
+                                      width, height, threshold, rate, counts.ctypes.data_as(C.c_void_p),
+                                      fail_at_firing, C.byref(ms)))
+    return out, counts, ms.value
 
 
 def validate_demo(which: int) -> int:

@@ -20,3 +20,9 @@ def test_delayed_self_loop_is_legal():
 def test_unknown_channel_is_build_error():
     assert H.validate_demo(3) == -1
     assert b"BuildError" in H.lib().dfh_last_error()
+
+
+def test_validate_cpu_actor_rules():
+    # A dynamic CPU actor (control tokens are consumed on the device, GPU
+    # actors only) and an actor with both a host and a device fire function.
+    assert H.validate_demo(4) == 2

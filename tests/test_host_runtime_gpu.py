@@ -70,3 +70,24 @@ def test_motion_acceptance6_through_runtime(gpu, hashes):
     for rate in (1, 4):
         got, _, _ = H.motion_run(f, h["w"], h["h"], 1, h["thr"], rate)
         assert hashlib.sha256(got.tobytes()).hexdigest() == h["out_sha256"]
+
+
+@pytest.mark.parametrize("w,h,rate", [(64, 48, 1), (320, 120, 3), (96, 40, 2)])
+def test_mixed_cpu_gpu_network(gpu, w, h, rate):
+    # CPU actors (gray, census) and the GPU motion actor on shared device
+    # channels: byte-exact masks, census counts from the CPU actor.
+    n = 4 * rate
+    rgb = O.synth_bytes(n * w * h * 3, 31 + w)
+    got, counts, _ = H.motion_run_mixed(rgb, w, h, 32, rate)
+    want = O.motion_rgb(rgb, w, h)
+    np.testing.assert_array_equal(got, want)
+    np.testing.assert_array_equal(counts, (want.reshape(n, -1) != 0).sum(1))
+
+
+def test_mixed_network_cpu_actor_fault(gpu):
+    # fire throwing at firing 3 ends the run in ActorFault naming the actor
+    # (proj/tests/test_runtime.cpp:251-277).
+    w, h = 64, 48
+    rgb = O.synth_bytes(8 * w * h * 3, 3)
+    with pytest.raises(H.HostRunError, match="ActorFault: actor 'census' faulted: census: injected fault"):
+        H.motion_run_mixed(rgb, w, h, 32, 1, fail_at_firing=3)
