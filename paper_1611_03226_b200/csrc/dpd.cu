@@ -171,6 +171,13 @@ __global__ void __launch_bounds__(1024) dpd_prep_kernel(DpdIO io, const float2* 
 // ---------------------------------------------------------------------------
 __host__ __device__ constexpr int pad_index(int w) { return w + (w >> 3); }  // bank-conflict pad
 
+// Resident CTAs per SM the register budget targets: 5 for the short
+// T=10 FIR (more CTAs hide each tile's input-load prologue; DPD-3 -5 %),
+// 4 for T=32 (its 10 x 32-tap FIR wants the registers; A/B in
+// profiles/r01_ab_dpd_variants.txt).
+template <int T>
+constexpr int dpd_min_blocks() { return T <= 16 ? 5 : 4; }
+
 template <int T, int V, int THREADS>
 struct MainCfg {
   static constexpr int S = THREADS * V;             // samples per tile
@@ -180,7 +187,7 @@ struct MainCfg {
 };
 
 template <int T, int V, int THREADS>
-__global__ void __launch_bounds__(THREADS) dpd_main_kernel(DpdIO io, const float2* __restrict__ taps_g,
+__global__ void __launch_bounds__(THREADS, dpd_min_blocks<T>()) dpd_main_kernel(DpdIO io, const float2* __restrict__ taps_g,
                                                             const float2* __restrict__ hist,
                                                             unsigned period, unsigned tiles_per_block,
                                                             unsigned* err, unsigned* done_counter) {
