@@ -172,11 +172,11 @@ __global__ void __launch_bounds__(1024) dpd_prep_kernel(DpdIO io, const float2* 
 __host__ __device__ constexpr int pad_index(int w) { return w + (w >> 3); }  // bank-conflict pad
 
 // Resident CTAs per SM the register budget targets: 5 for the short
-// T=10 FIR (more CTAs hide each tile's input-load prologue; DPD-3 -5 %),
-// 4 for T=32 (its 10 x 32-tap FIR wants the registers; A/B in
-// profiles/r01_ab_dpd_variants.txt).
+// T=10 FIR (more CTAs hide each tile's input-load prologue; DPD-3 -5 %);
+// unconstrained (0) for T=32, whose 10 x 32-tap FIR wants the registers
+// (A/B in profiles/r01_ab_dpd_variants.txt).
 template <int T>
-constexpr int dpd_min_blocks() { return T <= 16 ? 5 : 4; }
+constexpr int dpd_min_blocks() { return T <= 16 ? 5 : 0; }
 
 template <int T, int V, int THREADS>
 struct MainCfg {
