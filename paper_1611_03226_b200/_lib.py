@@ -130,6 +130,7 @@ _SIGS = {
     "df_motion_median5": (_i, [_vp, _vp, C.c_uint, C.c_uint, _vp]),
     "df_motion_rgb_to_gray": (_i, [_vp, _vp, _sz, _vp]),
     "df_motion_kernel_name": (C.c_char_p, [_vp]),
+    "df_launch_host_func": (_i, [_vp, _vp, _vp]),
     "df_peer_enable": (_i, [_i, _i]),
     "df_halo_copy": (_i, [_i, _vp, _i, _vp, _sz, _vp]),
     "df_fill_random_u8": (_i, [_vp, _sz, _u64, _vp]),
