@@ -238,16 +238,20 @@ __global__ void __launch_bounds__(THREADS, dpd_min_blocks<T>()) dpd_main_kernel(
   if (tile == 0) asm volatile("griddepcontrol.wait;" ::: "memory");  // history table from prep
   int prev_b = 1;
   int buf = 0;
+  // Window slot of position tid + m*THREADS: pad_index(tid) + m * (THREADS
+  // + THREADS/8) (THREADS % 8 == 0), so the stores use immediate offsets.
+  static_assert(THREADS % 8 == 0, "window padding");
+  const int pt = pad_index(tid);
+  // Block-start tiles: this thread's history entry for branch b is
+  // hb[(b - 1) * H1] (the prep kernel's table, u[-(tid+1)]).
+  const bool has_hist = tile == 0 && tid < H1;
+  const float2* hb = hist + ((size_t)p * kBranches * H1 + (has_hist ? tid : 0));
+  const int hslot = pad_index(H1 - 1 - (has_hist ? tid : 0));
 #pragma unroll 1
   for (uint32_t bits = mask; bits; bits &= bits - 1) {
     const int b = __ffs(bits);  // ascending branch order
-    // scale_b = scale_prev * mag^(b - prev): the reference's repeated
-    // product 1*mag*mag... (1*mag == mag exactly).
-    if (prev_b == 1 && b > 1) {
-#pragma unroll
-      for (int m = 0; m < C::M; ++m) sc[m] = mg[m];
-      prev_b = 2;
-    }
+    // scale_b = mag^(b-1) as the reference's repeated product from 1.0f
+    // (dpd.cpp:69-71); the first step 1.0f * mag == mag exactly.
 #pragma unroll 1
     for (; prev_b < b; ++prev_b) {
 #pragma unroll
@@ -259,14 +263,12 @@ __global__ void __launch_bounds__(THREADS, dpd_min_blocks<T>()) dpd_main_kernel(
       const int w = tid + m * THREADS;
       if (m < C::M - 1 || w < C::W) {
         // b == 1: sc = 1.0f and x * 1.0f == x exactly (no select needed)
-        u[pad_index(w)] = make_float2(__fmul_rn(xr[m], sc[m]), __fmul_rn(xi[m], sc[m]));
+        u[pt + m * (THREADS + THREADS / 8)] = make_float2(__fmul_rn(xr[m], sc[m]), __fmul_rn(xi[m], sc[m]));
       }
     }
-    if (tile == 0 && tid < H1) {
-      // History before the block start: the branch's frozen FIR state as
-      // resolved by the prep kernel (u[-(j+1)] at window index H1-1-j).
-      u[pad_index(H1 - 1 - tid)] = hist[((size_t)p * kBranches + (b - 1)) * H1 + tid];
-    }
+    // History before the block start: the branch's frozen FIR state as
+    // resolved by the prep kernel (u[-(j+1)] at window index H1-1-j).
+    if (has_hist) u[hslot] = hb[(b - 1) * H1];
     __syncthreads();
 
     // FIR over outputs o = tid*V + j (window index o + k' with k' = T-1-k).
