@@ -164,7 +164,8 @@ def test_raw_fire_and_config_actor_on_device(gpu):
     assert st.shape == (10, 9, 2)
 
 
-def test_channel_bound_firing(gpu):
+@pytest.mark.parametrize("T,period", [(10, 256), (32, 1000), (10, 5)])
+def test_channel_bound_firing(gpu, T, period):
     """Batched firing over device channels: control tokens and block tokens
     are consumed, and regions resolved, on the device."""
     from paper_1611_03226_b200 import dpd
@@ -172,10 +173,10 @@ def test_channel_bound_firing(gpu):
     from paper_1611_03226_b200.device import Stream
     import ctypes as C
     from paper_1611_03226_b200._lib import call
-    period, K, rounds = 256, 6, 5
+    K, rounds = 6, 5
     x = O.synth_samples(period * K * rounds, 21)
-    taps = O.random_taps(22)
-    sched = O.random_schedule(4, 23)
+    taps = O.random_taps(22, T)
+    sched = list(O.random_schedule(4, 23)) + [1, 0x200, 0]  # incl. k = 1 and empty masks
     s = Stream()
     ctrl = DeviceChannel(4, K)
     cin = DeviceChannel(8 * period, K)

@@ -114,6 +114,39 @@ def test_tma_tmem_band_heights(gpu, monkeypatch, ri, w, h, fmt, n, chunk):
     assert_frames_equal(run_gpu(f, w, h, fmt=fmt, chunk=chunk), want, w, h)
 
 
+def test_kernel_selection(gpu):
+    # 16-byte aligned rows take the TMA/TMEM kernel, the rest the
+    # register-prefetch kernel: both are exercised by this suite.
+    from paper_1611_03226_b200 import motion
+    assert motion.MotionActor(1280, 720, motion.RGB).kernel_name == "motion_m3_kernel"
+    assert motion.MotionActor(3840, 2160, motion.RGB).kernel_name == "motion_m3_kernel"
+    assert motion.MotionActor(320, 240, motion.GRAY).kernel_name == "motion_m3_kernel"
+    assert motion.MotionActor(488, 65, motion.RGB).kernel_name == "motion_fused_kernel"
+    assert motion.MotionActor(33, 29, motion.GRAY).kernel_name == "motion_fused_kernel"
+
+
+@pytest.mark.parametrize("h", [5, 6, 7, 53, 54, 55, 59, 60, 61, 108, 109, 113, 115])
+@pytest.mark.parametrize("ri", [0, 1, 2])
+def test_tma_tmem_heights_near_band_edges(gpu, monkeypatch, ri, h):
+    # Frame heights around the band heights (49/54/59): last bands of 1..R
+    # rows, bands entirely in the border, interior/general band mixes.
+    monkeypatch.setenv("DF_MOTION_M3_R", str(ri))
+    w, n = 256, 3
+    f = O.synth_bytes(n * w * h, 1000 * ri + h)
+    assert_frames_equal(run_gpu(f, w, h, chunk=2), O.motion_gray(f, w, h), w, h)
+
+
+@pytest.mark.parametrize("thr", [0, 1, 127, 128, 254, 255])
+def test_tma_tmem_thresholds_structured(gpu, thr):
+    w, h, n = 512, 140, 7
+    yy, xx = np.mgrid[0:h, 0:w]
+    rgb = np.stack([np.stack([(xx * 3 + yy + 13 * t) % 256, (xx + 2 * yy + 7 * t) % 256,
+                              (5 * xx + yy * 3 + 29 * t) % 256], -1) for t in range(n)]).astype(np.uint8)
+    rgb[3, 20:90, 100:400] = 255
+    f = rgb.reshape(-1)
+    assert_frames_equal(run_gpu(f, w, h, thr, fmt=3), O.motion_rgb(f, w, h, thr), w, h)
+
+
 def test_many_frames_temporal_chunks(gpu):
     # Enough frames that the kernel splits the firing into frame ranges,
     # each recomputing gauss(f0 - 1) on chip.
