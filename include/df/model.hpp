@@ -191,4 +191,22 @@ std::vector<Violation> validate(const NetworkGraph& net);
 std::size_t capacity_tokens(const ChannelSpec& spec);
 std::size_t capacity_bytes(const ChannelSpec& spec);
 
+// Channel buffer memory of a network (channel.cpp:194-208; what cmd_mem
+// prints, bench.cpp:145-164 / :491-525).  For a B200 network this is the
+// HBM the device channels allocate (the per-channel control blocks and
+// actor-private state such as FIR history are not channel buffers).
+struct MemoryReport {
+  struct Line {
+    std::string channel_id;
+    std::uint32_t token_rate = 0;
+    std::size_t token_size = 0;
+    bool has_delay = false;
+    std::size_t capacity_tokens = 0;
+    std::size_t capacity_bytes = 0;
+  };
+  std::vector<Line> channels;
+  std::size_t total_bytes = 0;
+};
+MemoryReport memory_bytes(const NetworkGraph& net);
+
 }  // namespace df

@@ -43,6 +43,15 @@ int dfh_motion_run_mixed(int device, const uint8_t* rgb_host, uint8_t* out_host,
                          unsigned height, uint8_t threshold, uint32_t token_rate, uint32_t* counts,
                          int64_t fail_at_firing, double* sink_active_ms);
 
+/* Channel buffer memory (cmd_mem, proj/src/bench.cpp:491-525), no device:
+ * app 0 = motion (width, height, token_rate), 1 = dpd (period).
+ * shape 0 = the B200 network this library runs; shape 1 = the reference's
+ * network shape (5 motion channels / 56 DPD channels) restated with this
+ * library's model types, whose Eq. 1 total must equal the reference's.
+ * Returns the channel count (or -1, dfh_last_error). */
+int dfh_memory(int app, unsigned width, unsigned height, uint32_t token_rate, uint32_t period, int shape,
+               uint64_t* total_bytes);
+
 /* Host-side rule checks (no device): builds the named reference network
  * shape and returns the number of validate() violations (0 = runnable);
  * -1 with dfh_last_error() on a BuildError / invalid_argument. */

@@ -121,6 +121,114 @@ int dfh_motion_run_mixed(int device, const uint8_t* rgb_host, uint8_t* out_host,
   });
 }
 
+int dfh_memory(int app, unsigned width, unsigned height, uint32_t rate, uint32_t period, int shape,
+               uint64_t* total_bytes) {
+  int n = -1;
+  int rc = guarded([&] {
+    using namespace df;
+    auto noop = [](FiringContext&) {};
+    NetworkGraph net;
+    if (shape == 0 && app == 0) {  // the B200 motion network (one firing's worth of frames shapes it)
+      std::vector<std::uint8_t> io(std::size_t(width) * height * rate);
+      motion::Params p;
+      p.width = width;
+      p.height = height;
+      p.token_rate = rate;
+      p.frames = rate;
+      p.input = io;
+      p.output = io;
+      net = motion::build_network(p);
+    } else if (shape == 0) {  // the B200 DPD network
+      std::vector<std::complex<float>> io(period), taps(100);
+      dpd::Params p;
+      p.period = period;
+      p.samples = period;
+      p.taps = taps;
+      p.schedule = {dpd::ConfigToken::first_n(2)};
+      p.input = io;
+      p.output = io;
+      net = dpd::build_network(p);
+    } else if (app == 0) {  // reference motion shape (motion.cpp:107-218)
+      const std::size_t S = std::size_t(width) * height;
+      std::vector<ChannelSpec> ch = {{"src_gauss", S, rate, false, {}},
+                                     {"gauss_thres_cur", S, rate, false, {}},
+                                     {"gauss_thres_prev", S, rate, true, {}},
+                                     {"thres_med", S, rate, false, {}},
+                                     {"med_sink", S, rate, false, {}}};
+      ActorBehavior b;
+      b.fire = noop;
+      auto port = [](PortDirection d, const char* c) { return PortSpec{d, PortKind::regular, c}; };
+      const auto in = PortDirection::input, out = PortDirection::output;
+      std::vector<ActorSpec> a = {
+          {"source", ActorKind::static_rate, {port(out, "src_gauss")}, b},
+          {"gauss", ActorKind::static_rate,
+           {port(in, "src_gauss"), port(out, "gauss_thres_cur"), port(out, "gauss_thres_prev")}, b},
+          {"thres", ActorKind::static_rate,
+           {port(in, "gauss_thres_prev"), port(in, "gauss_thres_cur"), port(out, "thres_med")}, b},
+          {"med", ActorKind::static_rate, {port(in, "thres_med"), port(out, "med_sink")}, b},
+          {"sink", ActorKind::static_rate, {port(in, "med_sink")}, b}};
+      net = build_network(a, ch);
+    } else {  // reference DPD shape (dpd.cpp:151-356): 44 float planes + 12 config channels
+      const std::size_t plane = std::size_t(period) * sizeof(float);
+      std::vector<ChannelSpec> ch;
+      auto pair = [&](const std::string& base) {
+        ch.push_back({base + "_re", plane, 1, false, {}});
+        ch.push_back({base + "_im", plane, 1, false, {}});
+      };
+      pair("src_split");
+      for (int b = 1; b <= 10; ++b) pair("split_b" + std::to_string(b));
+      for (int b = 1; b <= 10; ++b) pair("b" + std::to_string(b) + "_adder");
+      pair("adder_sink");
+      ch.push_back({"cfg_split", 4, 1, false, {}});
+      for (int b = 1; b <= 10; ++b) ch.push_back({"cfg_b" + std::to_string(b), 4, 1, false, {}});
+      ch.push_back({"cfg_adder", 4, 1, false, {}});
+      ActorBehavior st, dyn;
+      st.fire = noop;
+      dyn.fire = noop;
+      dyn.device_control = true;
+      const auto in = PortDirection::input, out = PortDirection::output;
+      auto reg = [](PortDirection d, const std::string& c) { return PortSpec{d, PortKind::regular, c}; };
+      std::vector<ActorSpec> a;
+      a.push_back({"source", ActorKind::static_rate, {reg(out, "src_split_re"), reg(out, "src_split_im")}, st});
+      std::vector<PortSpec> cfg_ports = {reg(out, "cfg_split")};
+      for (int b = 1; b <= 10; ++b) cfg_ports.push_back(reg(out, "cfg_b" + std::to_string(b)));
+      cfg_ports.push_back(reg(out, "cfg_adder"));
+      a.push_back({"config", ActorKind::static_rate, cfg_ports, st});
+      std::vector<PortSpec> split = {{in, PortKind::control, "cfg_split"}, reg(in, "src_split_re"),
+                                     reg(in, "src_split_im")};
+      for (int b = 1; b <= 10; ++b) {
+        split.push_back(reg(out, "split_b" + std::to_string(b) + "_re"));
+        split.push_back(reg(out, "split_b" + std::to_string(b) + "_im"));
+      }
+      a.push_back({"split", ActorKind::dynamic_rate, split, dyn});
+      for (int b = 1; b <= 10; ++b) {
+        const std::string t = std::to_string(b);
+        a.push_back({"branch" + t, ActorKind::dynamic_rate,
+                     {{in, PortKind::control, "cfg_b" + t}, reg(in, "split_b" + t + "_re"),
+                      reg(in, "split_b" + t + "_im"), reg(out, "b" + t + "_adder_re"),
+                      reg(out, "b" + t + "_adder_im")},
+                     dyn});
+      }
+      std::vector<PortSpec> adder = {{in, PortKind::control, "cfg_adder"}};
+      for (int b = 1; b <= 10; ++b) {
+        adder.push_back(reg(in, "b" + std::to_string(b) + "_adder_re"));
+        adder.push_back(reg(in, "b" + std::to_string(b) + "_adder_im"));
+      }
+      adder.push_back(reg(out, "adder_sink_re"));
+      adder.push_back(reg(out, "adder_sink_im"));
+      a.push_back({"adder", ActorKind::dynamic_rate, adder, dyn});
+      a.push_back({"sink", ActorKind::static_rate, {reg(in, "adder_sink_re"), reg(in, "adder_sink_im")}, st});
+      net = build_network(a, ch);
+    }
+    const auto v = validate(net);
+    if (!v.empty()) throw std::invalid_argument("network shape failed validation: " + v.front().message);
+    const MemoryReport r = memory_bytes(net);
+    if (total_bytes) *total_bytes = r.total_bytes;
+    n = (int)r.channels.size();
+  });
+  return rc == 0 ? n : -1;
+}
+
 int dfh_validate_demo(int which) {
   int n = -1;
   int rc = guarded([&] {

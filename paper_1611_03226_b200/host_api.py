@@ -33,6 +33,8 @@ def lib():
         L.dfh_motion_run_mixed.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint, C.c_uint,
                                            C.c_uint8, C.c_uint32, C.c_void_p, C.c_int64, C.POINTER(C.c_double)]
         L.dfh_validate_demo.argtypes = [C.c_int]
+        L.dfh_memory.argtypes = [C.c_int, C.c_uint, C.c_uint, C.c_uint32, C.c_uint32, C.c_int,
+                                 C.POINTER(C.c_uint64)]
         _h = L
     return _h
 
@@ -82,6 +84,17 @@ def motion_run_mixed(rgb: np.ndarray, width: int, height: int, threshold: int = 
                                       width, height, threshold, rate, counts.ctypes.data_as(C.c_void_p),
                                       fail_at_firing, C.byref(ms)))
     return out, counts, ms.value
+
+
+def memory(app: str, shape: str, width: int = 320, height: int = 240, rate: int = 1, period: int = 65536):
+    """(channel count, Eq. 1 buffer bytes) of a network shape -- cmd_mem.
+    app: 'motion' | 'dpd'; shape: 'b200' (this library's network) | 'reference'."""
+    tot = C.c_uint64(0)
+    n = lib().dfh_memory(0 if app == "motion" else 1, width, height, rate, period,
+                         0 if shape == "b200" else 1, C.byref(tot))
+    if n < 0:
+        raise HostRunError(lib().dfh_last_error().decode(errors="replace"))
+    return n, tot.value
 
 
 def validate_demo(which: int) -> int:

@@ -26,3 +26,20 @@ def test_validate_cpu_actor_rules():
     # A dynamic CPU actor (control tokens are consumed on the device, GPU
     # actors only) and an actor with both a host and a device fire function.
     assert H.validate_demo(4) == 2
+
+
+def test_cmd_mem_parity(hashes):
+    # cmd_mem (proj/src/bench.cpp:491-525): the reference network shapes
+    # restated with this library's model types give the reference's Eq. 1
+    # totals, pinned by the compiled reference (tests/golden).
+    golden = hashes["mem_totals"]
+    assert H.memory("motion", "reference", 320, 240, 1) == (5, golden["motion_320x240_r1"])
+    assert H.memory("dpd", "reference", period=65536) == (56, golden["dpd_p65536"])
+    # The B200 networks: src (2r) + delay self-loop (3*1+1) + sink (2r) tokens
+    # for motion; DPD: config (2 x 4 B), in + out planes interleaved (2 x 8 B
+    # x period each).
+    S = 320 * 240
+    for r in (1, 4):
+        assert H.memory("motion", "b200", 320, 240, r) == (3, 2 * r * S + 4 * S + 2 * r * S)
+    # DPD (batch 1): control (2 x 4 B) + input and output blocks (2 x 8 B x period each).
+    assert H.memory("dpd", "b200", period=65536) == (3, 2 * 4 + 2 * (2 * 8 * 65536))
