@@ -1097,10 +1097,14 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 #define DF_MOTION_M3 1
 #endif
 
-bool m3_eligible(const df_motion* m, const MotionIO& io) {
+bool m3_eligible(const df_motion* m, const MotionIO& io, int frames) {
   const void* base = io.channel_mode ? (const void*)io.in_ch.storage : (const void*)io.in;
+  // TMA row coordinates are int32: the mapped rows (H x frames, + halo) must fit.
+  const unsigned long long map_frames =
+      io.channel_mode ? chan_capacity_tokens(io.in_ch.rate, io.in_ch.has_delay) : (unsigned long long)frames;
   return DF_MOTION_M3 && m->m3_resident[0] > 0 && ((size_t)m->W * m->fmt) % 16 == 0 &&
-         (reinterpret_cast<uintptr_t>(base) & 15) == 0 && tensor_map_encoder() != nullptr;
+         (reinterpret_cast<uintptr_t>(base) & 15) == 0 && (unsigned long long)m->H * map_frames < (1ull << 31) - 256 &&
+         tensor_map_encoder() != nullptr;
 }
 
 // Band heights M3 is built for; launch_m3 picks the one whose grid fills
@@ -1184,7 +1188,7 @@ int launch_m3(df_motion* m, const MotionIO& io, int frames, cudaStream_t s) {
 
 int launch_motion(df_motion* m, const MotionIO& io, int frames, cudaStream_t s) {
   if (frames <= 0) return DF_OK;
-  if (m3_eligible(m, io))
+  if (m3_eligible(m, io, frames))
     return m->fmt == DF_MOTION_RGB ? launch_m3<DF_MOTION_RGB>(m, io, frames, s)
                                    : launch_m3<DF_MOTION_GRAY>(m, io, frames, s);
   const bool fast = (m->W % 8 == 0);
