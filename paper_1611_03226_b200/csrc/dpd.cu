@@ -33,6 +33,12 @@
 // either an earlier block's input (poly recomputed -- it is memoryless) or
 // the carried FirState, and writes a small per-(block, branch) history
 // table.  All blocks of the batch then run fully in parallel.
+// Fast path (period >= T-1, every BASELINE config): the history of block p
+// is the tail of ONE block -- the branch's last earlier active block q -- so
+// the main kernel resolves it itself: each block-start tile scans the
+// control tokens back from p with warp ballots, and the grid's last CTA
+// advances the FirState from the per-branch last active block (atomicMax).
+// One launch per batch, no history table.
 #include <algorithm>
 #include <cstring>
 #include <vector>
@@ -186,15 +192,28 @@ struct MainCfg {
   static constexpr int M = (W + THREADS - 1) / THREADS;  // poly positions per thread
 };
 
-template <int T, int V, int THREADS>
+// Fast-path state (see header): state = the carried FirState (read by
+// block-start tiles with no earlier active block, advanced in place by the
+// grid's last CTA); last1[b] = 1 + last active block of branch b+1 in the
+// batch (0: none), reset by the last CTA.
+struct FastState {
+  float2* state;
+  int* last1;
+};
+
+template <int T, int V, int THREADS, bool FAST>
 __global__ void __launch_bounds__(THREADS, dpd_min_blocks<T>()) dpd_main_kernel(DpdIO io, const float2* __restrict__ taps_g,
                                                             const float2* __restrict__ hist,
                                                             unsigned period, unsigned tiles_per_block,
-                                                            unsigned* err, unsigned* done_counter) {
+                                                            unsigned* err, unsigned* done_counter,
+                                                            FastState fs) {
   using C = MainCfg<T, V, THREADS>;
   constexpr int H1 = T - 1;
+  constexpr int HS = H1 > 0 ? H1 : 1;
   __shared__ float2 taps_s[kBranches * T];
   __shared__ float2 us[2][C::WP];
+  __shared__ float2 hist_s[FAST ? kBranches * HS : 1];  // fast path: this block's history per branch
+  __shared__ int q_s[kBranches];
 
   const unsigned long long p = blockIdx.y;
   const unsigned tile = blockIdx.x;
@@ -235,7 +254,45 @@ __global__ void __launch_bounds__(THREADS, dpd_min_blocks<T>()) dpd_main_kernel(
   float outr[V], outi[V];
 #pragma unroll
   for (int j = 0; j < V; ++j) outr[j] = outi[j] = -0.0f;
-  if (tile == 0) asm volatile("griddepcontrol.wait;" ::: "memory");  // history table from prep
+  constexpr bool fast = FAST;
+  if (fast && tile == 0 && mask && H1 > 0) {
+    // Last earlier active block per active branch: warp 0 scans the tokens
+    // back from p, 32 per step (lowest set lane = most recent block).
+    if (tid < 32) {
+      unsigned need = mask;
+      for (long long base = (long long)p; need && base > 0; base -= 32) {
+        const long long idx = base - 1 - tid;
+        const uint32_t m = idx >= 0 ? ctrl[idx] : 0u;
+        for (unsigned bits = need; bits; bits &= bits - 1) {
+          const int b = __ffs(bits);
+          const unsigned bal = __ballot_sync(0xffffffffu, (m >> (b - 1)) & 1u);
+          if (bal) {
+            if (tid == 0) q_s[b - 1] = (int)(base - __ffs(bal));
+            need &= ~(1u << (b - 1));
+          }
+        }
+      }
+      if (tid == 0)
+        for (unsigned bits = need; bits; bits &= bits - 1) q_s[__ffs(bits) - 1] = -1;
+      if (tid < kBranches && ((mask >> tid) & 1u)) atomicMax(&fs.last1[tid], (int)p + 1);
+    }
+    __syncthreads();
+    // hist_s[b][j] = u_b[-(j+1)]: poly of block q's sample period-1-j, or
+    // the carried FirState[j] when the branch has no earlier active block.
+    for (int it = tid; it < kBranches * H1; it += THREADS) {
+      const int bi = it / H1, j = it - bi * H1;
+      if (!((mask >> bi) & 1u)) continue;
+      const int q = q_s[bi];
+      if (q >= 0) {
+        const float2 v = __ldg(&x[(size_t)q * period + (period - 1 - j)]);
+        hist_s[it] = poly_sample(v.x, v.y, bi + 1);
+      } else {
+        hist_s[it] = fs.state[bi * (kMaxTaps - 1) + j];
+      }
+    }
+    __syncthreads();
+  }
+  if (!fast && tile == 0) asm volatile("griddepcontrol.wait;" ::: "memory");  // history table from prep
   int prev_b = 1;
   int buf = 0;
   // Window slot of position tid + m*THREADS: pad_index(tid) + m * (THREADS
@@ -245,7 +302,8 @@ __global__ void __launch_bounds__(THREADS, dpd_min_blocks<T>()) dpd_main_kernel(
   // Block-start tiles: this thread's history entry for branch b is
   // hb[(b - 1) * H1] (the prep kernel's table, u[-(tid+1)]).
   const bool has_hist = tile == 0 && tid < H1;
-  const float2* hb = hist + ((size_t)p * kBranches * H1 + (has_hist ? tid : 0));
+  const float2* hb = fast ? hist_s + (has_hist ? tid : 0)
+                          : hist + ((size_t)p * kBranches * H1 + (has_hist ? tid : 0));
   const int hslot = pad_index(H1 - 1 - (has_hist ? tid : 0));
 #pragma unroll 1
   for (uint32_t bits = mask; bits; bits &= bits - 1) {
@@ -323,13 +381,15 @@ __global__ void __launch_bounds__(THREADS, dpd_min_blocks<T>()) dpd_main_kernel(
     st[pad_index(tid * V + j)] = make_float2(__fadd_rn(outr[j], 0.0f), __fadd_rn(outi[j], 0.0f));
   __syncthreads();
   for (int o = tid; o < n; o += THREADS) y[blk + t0 + o] = st[pad_index(o)];
-  // Never complete before the prep grid (it also advances the FirState the
-  // next batch's prep reads).
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // The grid must not complete before the prep grid (which also advances
+  // the FirState the next batch's prep reads).  Block-start tiles already
+  // waited on it, and every batch has one, so no other CTA needs to: they
+  // retire and free their slots while prep may still be running.
 
-  if (io.channel_mode) {
-    // Last CTA commits the firing batch: K control tokens, K block tokens
-    // consumed, K block tokens produced (all ports always at full rate).
+  if (io.channel_mode || fast) {
+    // Last CTA: advances the FirState (fast path; every other CTA has read
+    // the old one) and commits the firing batch: K control tokens, K block
+    // tokens consumed, K block tokens produced (ports always at full rate).
     __shared__ bool last;
     __syncthreads();
     if (tid == 0) {
@@ -338,12 +398,27 @@ __global__ void __launch_bounds__(THREADS, dpd_min_blocks<T>()) dpd_main_kernel(
       last = atomicAdd(done_counter, 1u) == total - 1;
     }
     __syncthreads();
-    if (last && tid == 0) {
-      __threadfence();
+    if (!last) return;
+    __threadfence();
+    if (fast) {
+      for (int it = tid; it < kBranches * H1; it += THREADS) {
+        const int bi = it / H1, j = it - bi * H1;
+        const int q = *(volatile int*)&fs.last1[bi] - 1;
+        if (q >= 0) {
+          const float2 v = x[(size_t)q * period + (period - 1 - j)];
+          fs.state[bi * (kMaxTaps - 1) + j] = poly_sample(v.x, v.y, bi + 1);
+        }
+      }
+      __syncthreads();
+      if (tid < kBranches) fs.last1[tid] = 0;
+    }
+    if (tid == 0) {
       *done_counter = 0;
-      chan_commit_read(io.ctrl_ch, io.ctrl_ch.rate);
-      chan_commit_read(io.in_ch, io.in_ch.rate);
-      chan_commit_write(io.out_ch, io.out_ch.rate);
+      if (io.channel_mode) {
+        chan_commit_read(io.ctrl_ch, io.ctrl_ch.rate);
+        chan_commit_read(io.in_ch, io.in_ch.rate);
+        chan_commit_write(io.out_ch, io.out_ch.rate);
+      }
     }
   }
 }
@@ -436,6 +511,12 @@ __global__ void dpd_config_kernel(const uint16_t* __restrict__ sched, unsigned l
 #ifndef DF_DPD_THREADS
 #define DF_DPD_THREADS 128
 #endif
+#ifndef DF_DPD_FAST
+// Fast path for T=10 (bit 0) and T=32 (bit 1).  T=32 keeps the prep kernel:
+// its FAST instantiation allocates registers differently and runs DPD-5 5 %
+// slower (11.21 vs 10.68 ms, profiles/r01_ab_dpd_variants.txt).
+#define DF_DPD_FAST 1
+#endif
 constexpr int kV = DF_DPD_V;              // consecutive outputs per thread
 constexpr int kThreads = DF_DPD_THREADS;  // threads per CTA (tile = kV * kThreads samples)
 
@@ -450,7 +531,7 @@ struct df_dpd {
   uint32_t T = 10;
   float2* taps = nullptr;      // device, 10*T
   float2* state = nullptr;     // device, 10*(kMaxTaps-1): FirState per branch
-  unsigned* scratch = nullptr; // [0] error word, [1] done counter
+  unsigned* scratch = nullptr; // [0] error word, [1] done counter, [4..13] fast-path last1
   float2* hist = nullptr;      // device history table, capacity hist_blocks
   int* act = nullptr;          // device active lists, 10*hist_blocks
   unsigned long long hist_blocks = 0;
@@ -485,7 +566,15 @@ int launch_dpd(df_dpd* d, const DpdIO& io, unsigned long long K, cudaStream_t s)
   DF_TRY(ensure_hist(d, K));
   unsigned* err = d->scratch;
   unsigned* done = d->scratch + 1;
-  if (d->T > 1) {
+  // Fast path (see the header): T in {10, 32} and blocks at least T-1 long.
+  const bool fast = ((d->T == 10 && (DF_DPD_FAST & 1)) || (d->T == 32 && (DF_DPD_FAST & 2))) && d->period >= d->T - 1;
+  // (FAST is a template parameter: the prep-path kernel keeps its own code.)
+  FastState fs{};
+  if (fast) {
+    fs.state = d->state;
+    fs.last1 = reinterpret_cast<int*>(d->scratch + 4);
+  }
+  if (d->T > 1 && !fast) {
     dpd_prep_kernel<<<kBranches, 1024, 0, s>>>(io, d->state, d->state, d->hist, d->act, K, d->period,
                                                 (int)d->T, err);
     DF_TRY(after_launch("dpd_prep_kernel"));
@@ -515,12 +604,13 @@ int launch_dpd(df_dpd* d, const DpdIO& io, unsigned long long K, cudaStream_t s)
       attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
       attr[0].val.programmaticStreamSerializationAllowed = 1;
       lc.attrs = attr;
-      lc.numAttrs = 1;
-      cudaError_t le = d->T == 10
-                           ? cudaLaunchKernelEx(&lc, dpd_main_kernel<10, kV, kThreads>, sub, (const float2*)d->taps,
-                                                hist, d->period, tiles, err, done)
-                           : cudaLaunchKernelEx(&lc, dpd_main_kernel<32, kV, kThreads>, sub, (const float2*)d->taps,
-                                                hist, d->period, tiles, err, done);
+      lc.numAttrs = fast ? 0 : 1;  // PDL only behind the prep kernel
+      const float2* tp = d->taps;
+      cudaError_t le =
+          d->T == 10 ? (fast ? cudaLaunchKernelEx(&lc, dpd_main_kernel<10, kV, kThreads, true>, sub, tp, hist, d->period, tiles, err, done, fs)
+                             : cudaLaunchKernelEx(&lc, dpd_main_kernel<10, kV, kThreads, false>, sub, tp, hist, d->period, tiles, err, done, fs))
+                     : (fast ? cudaLaunchKernelEx(&lc, dpd_main_kernel<32, kV, kThreads, true>, sub, tp, hist, d->period, tiles, err, done, fs)
+                             : cudaLaunchKernelEx(&lc, dpd_main_kernel<32, kV, kThreads, false>, sub, tp, hist, d->period, tiles, err, done, fs));
       DF_CHECK_CUDA(le);
       DF_TRY(after_launch("dpd_main_kernel"));
     }
@@ -711,7 +801,7 @@ int df_dpd_run_host(df_dpd* d, const float* in_host, float* out_host, uint64_t s
   if (samples == 0) return DF_OK;
   DF_CHECK_CUDA(cudaSetDevice(d->device));
   const uint64_t blocks = samples / d->period;
-  if (chunk_blocks == 0) chunk_blocks = std::max<uint64_t>(1, (128ull << 20) / (8ull * d->period));
+  if (chunk_blocks == 0) chunk_blocks = df::Staging::chunk_units(blocks, 8ull * d->period, 128ull << 20);
   chunk_blocks = std::min(chunk_blocks, blocks);
   const size_t chunk_bytes = chunk_blocks * d->period * 8ull;
   cudaStream_t cs = as_stream(stream);

@@ -1346,7 +1346,7 @@ int df_motion_run_host(df_motion* m, const void* in_host, uint8_t* out_host, uin
   if (frames == 0) return DF_OK;
   DF_CHECK_CUDA(cudaSetDevice(m->device));
   const size_t in_frame = (size_t)m->W * m->H * m->fmt, out_frame = (size_t)m->W * m->H;
-  if (chunk_frames == 0) chunk_frames = (uint32_t)std::max<size_t>(1, (256ull << 20) / in_frame);
+  if (chunk_frames == 0) chunk_frames = (uint32_t)df::Staging::chunk_units(frames, in_frame, 256ull << 20);
   chunk_frames = (uint32_t)std::min<uint64_t>(chunk_frames, frames);
   cudaStream_t cs = as_stream(stream);
   DF_TRY(m->staging.ensure(chunk_frames * in_frame, chunk_frames * out_frame));
