@@ -116,7 +116,17 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and BACKEND == "gloo":
+        # Functional check of the N>1 path on a box with fewer GPUs than
+        # ranks (gloo cannot see CUDA memory; halos are staged on the host).
+        import torch
+        local %= max(1, torch.cuda.device_count())
     return rank, world, local
+
+
+# Process-group backend: NCCL (P2P over NVLink) for every measured run;
+# DF_BENCH_BACKEND=gloo only for functional checks of the multi-rank path.
+BACKEND = os.environ.get("DF_BENCH_BACKEND", "nccl")
 
 
 def traffic_from_profiles(kernel: str, workload: str):
@@ -134,7 +144,7 @@ def bench_motion_ours(args, p, rank, world, local):
     import torch
     import torch.distributed as dist
 
-    from paper_1611_03226_b200 import _lib, device, motion
+    from paper_1611_03226_b200 import _lib, device, motion, shard
 
     _lib.require_gpu()
     torch.cuda.set_device(local)
@@ -153,13 +163,7 @@ def bench_motion_ours(args, p, rank, world, local):
         sh = C.c_void_p(torch.cuda.current_stream().cuda_stream)  # the capture stream inside a graph
         if world > 1:
             # One-frame halo: the previous rank's last input frame (NCCL P2P).
-            ops = []
-            if rank + 1 < world:
-                ops.append(dist.P2POp(dist.isend, inp[(F - 1) * in_frame:], rank + 1))
-            if rank > 0:
-                ops.append(dist.P2POp(dist.irecv, halo, rank - 1))
-            for r in dist.batch_isend_irecv(ops):
-                r.wait()
+            shard.exchange_tail(inp[(F - 1) * in_frame:], halo, rank, world)
         if rank > 0:
             _lib.call("df_motion_set_prev_frame", actor.handle, C.c_void_p(halo.data_ptr()), sh)
         else:
@@ -264,7 +268,7 @@ def max_over_ranks(x: float, world: int) -> float:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device="cpu" if BACKEND == "gloo" else "cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -568,7 +572,10 @@ def main():
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if BACKEND == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     res = (bench_motion_ours if kind == "motion" else bench_dpd_ours)(args, p, rank, world, local)
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:

@@ -40,12 +40,19 @@ def exchange_tail(send_tail, recv_buf, rank: int, world: int):
     """Rank r sends `send_tail` (its last frame / last T-1 samples) to r+1 and
     receives r-1's into `recv_buf`.  Returns True if a halo was received."""
     import torch.distributed as dist
+    staged = dist.get_backend() == "gloo" and (send_tail.is_cuda or recv_buf.is_cuda)
+    if staged:  # gloo moves host memory only (functional checks of device runs)
+        send_t, recv_t = send_tail.cpu(), recv_buf.new_empty(recv_buf.shape, device="cpu")
+    else:
+        send_t, recv_t = send_tail, recv_buf
     ops = []
     if rank + 1 < world:
-        ops.append(dist.P2POp(dist.isend, send_tail, rank + 1))
+        ops.append(dist.P2POp(dist.isend, send_t, rank + 1))
     if rank > 0:
-        ops.append(dist.P2POp(dist.irecv, recv_buf, rank - 1))
+        ops.append(dist.P2POp(dist.irecv, recv_t, rank - 1))
     if ops:
         for req in dist.batch_isend_irecv(ops):
             req.wait()
+    if staged and rank > 0:
+        recv_buf.copy_(recv_t)
     return rank > 0

@@ -94,6 +94,26 @@ def test_chunked_firings_equal_one_batch(gpu):
         assert_parity(run_gpu(x, taps, sched, period, chunk_blocks=chunk), want)
 
 
+@pytest.mark.parametrize("T", [10, 32])
+@pytest.mark.parametrize("chunk", [0, 7, 64])
+def test_long_gated_off_stretches(gpu, T, chunk):
+    """Branches gated off for 32..150 blocks, inactive in whole firing
+    batches, and never active: the frozen history must come from the last
+    active block far back (several 32-token ballot steps of the in-kernel
+    scan), from the carried FirState across batches, or stay zero
+    (proj/src/dpd.cpp:264-279)."""
+    period, blocks = 64, 200
+    sched = np.full(blocks, 0x001, np.uint16)  # branch 1 always on
+    sched[[0, 150, 151]] |= 1 << 4             # branch 5: gap of 149 blocks
+    sched[[3, 35, 67, 199]] |= 1 << 6          # branch 7: gaps of exactly 32
+    sched[[40, 41, 42]] |= 1 << 8              # branch 9: active once, gated after
+    # branch 10 never active; branch 2 active only in the last block
+    sched[199] |= 1 << 1
+    x = O.synth_samples(period * blocks, 2024 + T)
+    taps = O.random_taps(90 + T, T)
+    assert_parity(run_gpu(x, taps, sched, period, chunk_blocks=chunk), O.dpd(x, taps, sched, period))
+
+
 def test_gating_invariance_acceptance9(gpu):
     # proj/tests/acceptance.cpp:398-450: branch 7 toggled; inactive periods
     # must be bit-identical when its taps change.
