@@ -124,9 +124,45 @@ def dist_env():
     return rank, world, local
 
 
-# Process-group backend: NCCL (P2P over NVLink) for every measured run;
-# DF_BENCH_BACKEND=gloo only for functional checks of the multi-rank path.
+# Process-group backend: NCCL for every measured run; DF_BENCH_BACKEND=gloo
+# only for functional checks of the multi-rank path.
 BACKEND = os.environ.get("DF_BENCH_BACKEND", "nccl")
+# Halo transport at N>1: "ipc" (default) -- rank r maps rank r-1's shard
+# buffer once (CUDA IPC) and pulls each step's halo with a copy-engine peer
+# copy over NVLink on a side stream, overlapped with the previous step's
+# kernel; "p2p" -- NCCL send/recv on the compute stream.
+HALO = os.environ.get("DF_BENCH_HALO", "ipc")
+
+
+class HaloPipe:
+    """Double-buffered halo pulls on a side stream (peer copies
+    overlapped with interior work).  pull(i, copies) issues step i's copies
+    [(dst_ptr_fn(slot), src_ptr, bytes)], and makes `stream` wait for them;
+    release(i) marks step i's slot consumed (after its consumer kernel)."""
+
+    def __init__(self, torch, stream, local, peer_device):
+        self.torch, self.stream, self.local, self.peer = torch, stream, local, peer_device
+        self.hs = torch.cuda.Stream()
+        self.ready = [torch.cuda.Event(), torch.cuda.Event()]
+        self.free = [torch.cuda.Event(), torch.cuda.Event()]
+        self.used = [False, False]
+
+    def pull(self, i, copies):
+        from paper_1611_03226_b200 import _lib
+        k = i % 2
+        with self.torch.cuda.stream(self.hs):
+            if self.used[k]:
+                self.hs.wait_event(self.free[k])
+            hsh = C.c_void_p(self.hs.cuda_stream)
+            for dst, src, nbytes in copies:
+                _lib.call("df_halo_copy", self.local, C.c_void_p(dst), self.peer, C.c_void_p(src), nbytes, hsh)
+            self.ready[k].record(self.hs)
+        self.stream.wait_event(self.ready[k])
+        return k
+
+    def release(self, k):
+        self.free[k].record(self.stream)
+        self.used[k] = True
 
 
 def traffic_from_profiles(kernel: str, workload: str):
@@ -153,19 +189,37 @@ def bench_motion_ours(args, p, rank, world, local):
     in_frame, out_frame = W * H * fmt, W * H
     stream = torch.cuda.current_stream()
     sh = C.c_void_p(stream.cuda_stream)
-    inp = torch.empty(F * in_frame, dtype=torch.uint8, device=dev)
+    inp_buf = device.Buffer(F * in_frame, local)  # cudaMalloc'ed: exportable to the neighbour rank
+    inp = inp_buf.as_tensor()
     out = torch.empty(F * out_frame, dtype=torch.uint8, device=dev)
-    halo = torch.empty(in_frame, dtype=torch.uint8, device=dev)
+    halos = [torch.empty(in_frame, dtype=torch.uint8, device=dev) for _ in range(2)]
     _lib.call("df_fill_random_u8", C.c_void_p(inp.data_ptr()), inp.numel(), 1234 + rank, sh)
     actor = motion.MotionActor(W, H, fmt, p["thr"], device=local)
+    peer = pipe = None
+    if world > 1:
+        torch.cuda.synchronize()
+        dist.barrier()  # every shard is filled before a neighbour maps it
+        if HALO == "ipc":
+            peer = shard.PeerBuffer(inp.data_ptr(), local, rank, world)
+            if rank > 0:
+                pipe = HaloPipe(torch, stream, local, peer.device)
+    nstep = [0]
 
     def step(ev_k0=None, ev_k1=None):
         sh = C.c_void_p(torch.cuda.current_stream().cuda_stream)  # the capture stream inside a graph
+        k = 0
         if world > 1:
-            # One-frame halo: the previous rank's last input frame (NCCL P2P).
-            shard.exchange_tail(inp[(F - 1) * in_frame:], halo, rank, world)
+            # One-frame halo: the previous rank's last input frame.
+            if pipe is not None:
+                k = pipe.pull(nstep[0], [(halos[nstep[0] % 2].data_ptr(), peer.ptr + (F - 1) * in_frame,
+                                          in_frame)])
+            elif HALO != "ipc":
+                shard.exchange_tail(inp[(F - 1) * in_frame:], halos[0], rank, world)
+        nstep[0] += 1
         if rank > 0:
-            _lib.call("df_motion_set_prev_frame", actor.handle, C.c_void_p(halo.data_ptr()), sh)
+            _lib.call("df_motion_set_prev_frame", actor.handle, C.c_void_p(halos[k].data_ptr()), sh)
+            if pipe is not None:
+                pipe.release(k)
         else:
             _lib.call("df_motion_set_prev_frame", actor.handle, None, sh)
         if ev_k0 is not None:
@@ -225,6 +279,9 @@ def bench_motion_ours(args, p, rank, world, local):
         e2e_t.append(time.perf_counter() - a)
     e2e_s = max_over_ranks(statistics.median(e2e_t), world)
     torch.cuda.synchronize()
+    if peer is not None:  # unmap the neighbour's shard before anyone frees theirs
+        peer.close()
+        dist.barrier()
 
     value = world * F / (ms / 1e3)
     bytes_alg = 4.0 * W * H * F if fmt == 3 else 2.0 * W * H * F
@@ -248,7 +305,8 @@ def bench_motion_ours(args, p, rank, world, local):
         "config": {"workload": p["label"], "width": W, "height": H, "frames_per_gpu": F,
                    "threshold": p["thr"], "input": "rgb" if fmt == 3 else "gray",
                    "chain": "gray->gauss5x5->|cur-prev|>thr->median5 (reference-pinned)",
-                   "parallelism": f"frame-range shards x{world}, 1-frame halo via NCCL P2P",
+                   "parallelism": f"frame-range shards x{world}, 1-frame halo via "
+                                  + ("NVLink peer copy (CUDA IPC), overlapped" if HALO == "ipc" else "NCCL P2P"),
                    "l2": f"inputs {F * in_frame / 1e6:.0f} MB per GPU > 126 MB L2 (no flush needed)"},
         "e2e": {"value": round(world * F / e2e_s, 1), "unit": "frames/s",
                 "h2d_bytes_per_step": F * in_frame, "d2h_bytes_per_step": F * out_frame,
@@ -307,7 +365,8 @@ def bench_dpd_ours(args, p, rank, world, local):
     sched = dpd_schedule(p["sched"], blocks)
     stream = torch.cuda.current_stream()
     sh = C.c_void_p(stream.cuda_stream)
-    x = torch.empty(2 * N, dtype=torch.float32, device=dev)
+    x_buf = device.Buffer(8 * N, local)  # cudaMalloc'ed: exportable to the neighbour rank
+    x = x_buf.as_tensor(np.float32)
     y = torch.empty(2 * N, dtype=torch.float32, device=dev)
     ctrl = torch.empty(blocks, dtype=torch.int32, device=dev)
     _lib.call("df_fill_random_pm1", C.c_void_p(x.data_ptr()), 2 * N, 99 + rank, sh)
@@ -320,28 +379,47 @@ def bench_dpd_ours(args, p, rank, world, local):
     # Block-range shard of a weak-scaled stream: rank r holds blocks
     # [r*blocks, (r+1)*blocks).  FIR-history halo: for each branch, the last
     # T-1 samples of its last active block in the previous rank's range
-    # (NCCL P2P, no collective); rank 0 starts from zero history.
+    # (peer copies of the neighbour's mapped shard, or NCCL P2P; no
+    # collective); rank 0 starts from zero history.
     from paper_1611_03226_b200 import shard
     H1 = max(T - 1, 1)
     tails = torch.zeros(10 * H1 * 2, dtype=torch.float32, device=dev)
-    halo = torch.zeros_like(tails)
+    halos = [torch.zeros_like(tails) for _ in range(2)]
     tail_src = []
     for b in range(1, 11):
         hb = shard.dpd_halo_block(sched, blocks, b)  # last active block of this rank (local index)
         tail_src.append(hb)
+    peer = pipe = None
+    if world > 1:
+        torch.cuda.synchronize()
+        dist.barrier()  # every shard is filled before a neighbour maps it
+        if HALO == "ipc":
+            peer = shard.PeerBuffer(x.data_ptr(), local, rank, world)
+            if rank > 0:
+                pipe = HaloPipe(torch, stream, local, peer.device)
+    nstep = [0]
 
     def step(ev0=None, ev1=None):
         sh = C.c_void_p(torch.cuda.current_stream().cuda_stream)  # the capture stream inside a graph
         if world > 1:
-            for b, hb in enumerate(tail_src):
-                if hb is not None:
-                    a0 = 2 * ((hb + 1) * period - H1)
-                    tails[2 * H1 * b: 2 * H1 * (b + 1)].copy_(x[a0: a0 + 2 * H1])
-            got = shard.exchange_tail(tails, halo, rank, world)
+            k, got = 0, rank > 0
+            if pipe is not None:
+                k = nstep[0] % 2
+                pipe.pull(nstep[0], [(halos[k].data_ptr() + 8 * H1 * b, peer.ptr + 8 * ((hb + 1) * period - H1),
+                                      8 * H1) for b, hb in enumerate(tail_src) if hb is not None])
+            elif HALO != "ipc":
+                for b, hb in enumerate(tail_src):
+                    if hb is not None:
+                        a0 = 2 * ((hb + 1) * period - H1)
+                        tails[2 * H1 * b: 2 * H1 * (b + 1)].copy_(x[a0: a0 + 2 * H1])
+                got = shard.exchange_tail(tails, halos[0], rank, world)
             if got:
                 for b in range(10):
-                    _lib.call("df_dpd_set_history", actor.handle, C.c_void_p(halo.data_ptr() + 8 * H1 * b), H1,
+                    _lib.call("df_dpd_set_history", actor.handle, C.c_void_p(halos[k].data_ptr() + 8 * H1 * b), H1,
                               1 << b, sh)
+                if pipe is not None:
+                    pipe.release(k)
+        nstep[0] += 1
         if ev0 is not None:
             ev0.record(stream)
         _lib.call("df_dpd_fire", actor.handle, C.c_void_p(ctrl.data_ptr()), C.c_void_p(x.data_ptr()),
@@ -390,6 +468,10 @@ def bench_dpd_ours(args, p, rank, world, local):
         actor.run_host(hin.array, hout.array, sched)
         e2e_t.append(time.perf_counter() - a)
     e2e_s = max_over_ranks(statistics.median(e2e_t), world)
+    if peer is not None:  # unmap the neighbour's shard before anyone frees theirs
+        torch.cuda.synchronize()
+        peer.close()
+        dist.barrier()
 
     fps = dpd_flops_per_sample(sched, T)
     achieved_tops = N * fps / (kms / 1e3) / 1e12
@@ -403,7 +485,8 @@ def bench_dpd_ours(args, p, rank, world, local):
         "data": "synthetic (device uniform[-1,1) complex samples)",
         "config": {"workload": p["label"], "samples_per_gpu": N, "period": period, "taps_per_branch": T,
                    "schedule": p["sched"],
-                   "parallelism": f"block-range shards x{world}, per-branch FIR-history halo via NCCL P2P",
+                   "parallelism": f"block-range shards x{world}, per-branch FIR-history halo via "
+                                  + ("NVLink peer copies (CUDA IPC), overlapped" if HALO == "ipc" else "NCCL P2P"),
                    "l2": f"in+out {16 * N / 1e6:.0f} MB per GPU"},
         "e2e": {"value": round(world * N / e2e_s / 1e6, 1), "unit": "Msamples/s",
                 "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * N,

@@ -258,6 +258,14 @@ int df_motion_rgb_to_gray(const uint8_t* rgb_dev, uint8_t* gray_dev, size_t pixe
 int df_peer_enable(int device_a, int device_b);
 int df_halo_copy(int dst_device, void* dst, int src_device, const void* src, size_t bytes,
                  void* stream);
+/* One process per GPU: export a cudaMalloc'ed shard buffer (handle of
+ * df_ipc_handle_size() bytes), map a neighbour's exported buffer (peer
+ * access enabled lazily), and unmap it.  The mapped pointer is a peer
+ * pointer for df_halo_copy (src_device = the exporting rank's device). */
+int df_ipc_handle_size(void);
+int df_ipc_get_handle(const void* dev_ptr, void* handle_out);
+int df_ipc_open_handle(int device, const void* handle, void** dev_ptr);
+int df_ipc_close_handle(void* dev_ptr);
 
 /* ---- synthetic inputs on device (bench data; not the reference streams) */
 int df_fill_random_u8(void* dst, size_t bytes, uint64_t seed, void* stream);

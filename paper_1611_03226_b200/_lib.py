@@ -133,6 +133,10 @@ _SIGS = {
     "df_launch_host_func": (_i, [_vp, _vp, _vp]),
     "df_peer_enable": (_i, [_i, _i]),
     "df_halo_copy": (_i, [_i, _vp, _i, _vp, _sz, _vp]),
+    "df_ipc_handle_size": (_i, []),
+    "df_ipc_get_handle": (_i, [_vp, _vp]),
+    "df_ipc_open_handle": (_i, [_i, _vp, _P(_vp)]),
+    "df_ipc_close_handle": (_i, [_vp]),
     "df_fill_random_u8": (_i, [_vp, _sz, _u64, _vp]),
     "df_fill_random_pm1": (_i, [_vp, _sz, _u64, _vp]),
     "df_kernel_launches": (_u64, []),

@@ -202,6 +202,30 @@ int df_halo_copy(int dst_device, void* dst, int src_device, const void* src, siz
   return DF_OK;
 }
 
+// Cross-process peer memory (one process per GPU): a rank exports its
+// shard's allocation once, its neighbour maps it and pulls the halo with
+// copy-engine peer copies over NVLink -- no collective, no NCCL kernel.
+int df_ipc_handle_size(void) { return (int)sizeof(cudaIpcMemHandle_t); }
+int df_ipc_get_handle(const void* dev_ptr, void* handle_out) {
+  DF_REQUIRE(dev_ptr && handle_out, DF_EINVAL, "df_ipc_get_handle: null argument");
+  cudaIpcMemHandle_t h;
+  DF_CHECK_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
+  std::memcpy(handle_out, &h, sizeof h);
+  return DF_OK;
+}
+int df_ipc_open_handle(int device, const void* handle, void** dev_ptr) {
+  DF_REQUIRE(handle && dev_ptr, DF_EINVAL, "df_ipc_open_handle: null argument");
+  DF_CHECK_CUDA(cudaSetDevice(device));
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof h);
+  DF_CHECK_CUDA(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return DF_OK;
+}
+int df_ipc_close_handle(void* dev_ptr) {
+  DF_CHECK_CUDA(cudaIpcCloseMemHandle(dev_ptr));
+  return DF_OK;
+}
+
 int df_fill_random_u8(void* dst, size_t bytes, uint64_t seed, void* stream) {
   DF_REQUIRE(dst || bytes == 0, DF_EINVAL, "df_fill_random_u8: null destination");
   if (bytes == 0) return DF_OK;

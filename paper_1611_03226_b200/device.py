@@ -106,6 +106,17 @@ class Buffer:
     def at(self, offset: int) -> C.c_void_p:
         return C.c_void_p(self.ptr.value + offset)
 
+    def as_tensor(self, dtype=np.uint8):
+        """Zero-copy torch view (CUDA array interface) of the allocation;
+        the Buffer must outlive it."""
+        import torch
+        dt = np.dtype(dtype)
+
+        class _View:
+            __cuda_array_interface__ = {"shape": (self.nbytes // dt.itemsize,), "typestr": dt.str,
+                                        "data": (self.ptr.value, False), "version": 3}
+        return torch.as_tensor(_View(), device=f"cuda:{self.device}")
+
     def free(self):
         if self.ptr:
             call("df_free", self.ptr)

@@ -56,3 +56,37 @@ def exchange_tail(send_tail, recv_buf, rank: int, world: int):
     if staged and rank > 0:
         recv_buf.copy_(recv_t)
     return rank > 0
+
+
+class PeerBuffer:
+    """Rank r's view of rank r-1's exported shard buffer (CUDA IPC): set up
+    once (handles travel by all_gather_object -- setup, not the data path);
+    halos are then pulled with copy-engine peer copies over NVLink
+    (df_halo_copy), off the compute stream."""
+
+    def __init__(self, ptr: int, device: int, rank: int, world: int):
+        import ctypes as C
+
+        import torch.distributed as dist
+
+        from . import _lib
+        n = _lib.lib().df_ipc_handle_size()
+        h = (C.c_char * n)()
+        _lib.call("df_ipc_get_handle", C.c_void_p(ptr), h)
+        mine = (bytes(h), device)
+        every = [None] * world
+        dist.all_gather_object(every, mine)
+        self.ptr = None
+        self.device = None
+        if rank > 0:
+            handle, self.device = every[rank - 1]
+            hb = (C.c_char * n).from_buffer_copy(handle)
+            p = C.c_void_p()
+            _lib.call("df_ipc_open_handle", device, hb, C.byref(p))
+            self.ptr = p.value
+
+    def close(self):
+        if self.ptr:
+            from . import _lib
+            _lib.call("df_ipc_close_handle", __import__("ctypes").c_void_p(self.ptr))
+            self.ptr = None

@@ -1,0 +1,123 @@
+"""GPU, world size 2 (two processes on cuda:0, gloo for setup only): the
+N>1 transport of bench.py -- each rank exports its shard buffer once (CUDA
+IPC), the next rank maps it and pulls its halo with a copy-engine peer copy
+(df_halo_copy), then fires its shard through the C ABI.  The concatenated
+shard outputs must equal the oracle on the unsharded stream, byte for byte
+(motion: frame-range shards, one-frame halo) and bit for bit (DPD:
+block-range shards, per-branch FIR-history halos, dynamic schedule)."""
+import ctypes as C
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _motion_worker(rank, world, port, q):
+    from paper_1611_03226_b200 import _lib, device, motion, shard
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        w, h, n = 160, 48, 12
+        fb = w * h * 3
+        rgb = O.synth_bytes(n * fb, 4242)
+        f0, f1 = shard.frame_shards(n, world)[rank]
+        mine = device.Buffer.from_array(rgb[f0 * fb:f1 * fb])
+        dist.barrier()
+        peer = shard.PeerBuffer(mine.ptr.value, 0, rank, world)
+        actor = motion.MotionActor(w, h, motion.RGB, 32)
+        if rank > 0:
+            halo = device.Buffer(fb)
+            prev_frames = shard.frame_shards(n, world)[rank - 1]
+            last = (prev_frames[1] - prev_frames[0] - 1) * fb
+            _lib.call("df_halo_copy", 0, halo.ptr, peer.device, C.c_void_p(peer.ptr + last), fb, None)
+            _lib.call("df_motion_set_prev_frame", actor.handle, halo.ptr, None)
+        out = device.Buffer((f1 - f0) * w * h)
+        _lib.call("df_motion_fire", actor.handle, mine.ptr, out.ptr, f1 - f0, None)
+        q.put((rank, out.download(np.uint8)))
+        peer.close()
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def _dpd_worker(rank, world, port, q):
+    from paper_1611_03226_b200 import _lib, device, dpd, shard
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        period, blocks, T = 256, 24, 10
+        x = O.synth_samples(period * blocks, 31)
+        taps = O.random_taps(32, T)
+        sched = np.array([0x001, 0x3FF, 0x0F0, 0x2A5, 0x100, 0x003, 0x200], np.uint16)
+        s0, s1 = shard.block_shards(period * blocks, period, world)[rank]
+        b0, nb = s0 // period, (s1 - s0) // period
+        mine = device.Buffer.from_array(x[2 * s0:2 * s1])
+        ctrl = device.Buffer(4 * nb)
+        dpd.config_tokens(sched, b0, nb, ctrl)  # global block indices: the schedule cycles per block
+        dist.barrier()
+        peer = shard.PeerBuffer(mine.ptr.value, 0, rank, world)
+        actor = dpd.DpdActor(period, taps)
+        if rank > 0:
+            # Per branch: the tail of its last active block before this shard
+            # (on the previous rank here: every branch fires in its range).
+            p0 = shard.block_shards(period * blocks, period, world)[rank - 1][0] // period
+            halo = device.Buffer(8 * (T - 1))
+            for b in range(1, 11):
+                hb = shard.dpd_halo_block(sched, b0, b)
+                assert hb is not None and hb >= p0
+                src = peer.ptr + 8 * ((hb - p0 + 1) * period - (T - 1))
+                _lib.call("df_halo_copy", 0, halo.ptr, peer.device, C.c_void_p(src), 8 * (T - 1), None)
+                _lib.call("df_dpd_set_history", actor.handle, halo.ptr, T - 1, 1 << (b - 1), None)
+        out = device.Buffer(8 * (s1 - s0))
+        actor.fire(ctrl, mine, out, nb)
+        actor.check()
+        q.put((rank, out.download(np.float32)))
+        peer.close()
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(worker, world=2):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return np.concatenate([got[r] for r in range(world)])
+
+
+def test_motion_frame_shards_ipc_halo(gpu):
+    w, h, n = 160, 48, 12
+    rgb = O.synth_bytes(n * w * h * 3, 4242)
+    np.testing.assert_array_equal(_run(_motion_worker), O.motion_rgb(rgb, w, h, 32))
+
+
+def test_dpd_block_shards_ipc_halo(gpu):
+    period, blocks, T = 256, 24, 10
+    x = O.synth_samples(period * blocks, 31)
+    taps = O.random_taps(32, T)
+    sched = np.array([0x001, 0x3FF, 0x0F0, 0x2A5, 0x100, 0x003, 0x200], np.uint16)
+    want = O.dpd(x, taps, sched, period)
+    got = _run(_dpd_worker)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
