@@ -588,6 +588,13 @@ constexpr size_t kSmemBytes = sizeof(uint2) * kWarpsPerCta * (kBandRows + 2) * 3
 #ifndef DF_M3_ST
 #define DF_M3_ST 3
 #endif
+// Shared-memory row loads issued at the start of a step (before the
+// gauss/thres/median work) instead of right before their use: A/B
+// (profiles/r01_ab_motion_variants.txt) 4K R=59 -1.8 %, 720p R=54 +1.3 %
+// (ptxas allocates R=54 at the 128-register cap), so per band height.
+#ifndef DF_M3_EARLY_MIN_R
+#define DF_M3_EARLY_MIN_R 59
+#endif
 constexpr int kM3Warps = 4;
 // Band heights R (template parameter): a frame pass fetches rows y0-3 ..
 // y0+R+2 (R + 6 rows, whole 5-row boxes), gauss(prev) holds R + 2 rows in
@@ -731,19 +738,26 @@ __device__ __forceinline__ void m3_pass(M3Stream<FMT, R>& st, unsigned char* __r
   if (MODE != 0) tmem_wait_st();
 
   // Row k (0..4) of the current group: the group is acquired at k == 0 and
-  // released at k == 4.
-  auto produce = [&](M3Row& r, int k) {
+  // released at k == 4.  fetch() reads the row's words from the ring;
+  // finish() converts them (split so a step can issue its shared-memory
+  // loads before the gauss/thres/median work that hides their latency).
+  auto fetch = [&](int k, uint2 (&w)[3]) {
     if (k == 0) st.acquire();
     const unsigned a = st.row(k);
+    w[0] = lds64(a);
+    if (FMT == DF_MOTION_RGB) {
+      w[1] = lds64(a + 8);
+      w[2] = lds64(a + 16);
+    }
+  };
+  auto finish = [&](M3Row& r, int k, const uint2 (&w)[3]) {
     unsigned g0, g1;
     if (FMT == DF_MOTION_RGB) {
-      const uint2 w0 = lds64(a), w1 = lds64(a + 8), w2 = lds64(a + 16);
-      g0 = rgb4_to_gray(w0.x, w0.y, w1.x, g.wg);
-      g1 = rgb4_to_gray(w1.y, w2.x, w2.y, g.wg);
+      g0 = rgb4_to_gray(w[0].x, w[0].y, w[1].x, g.wg);
+      g1 = rgb4_to_gray(w[1].y, w[2].x, w[2].y, g.wg);
     } else {
-      const uint2 w0 = lds64(a);
-      g0 = w0.x;
-      g1 = w0.y;
+      g0 = w[0].x;
+      g1 = w[0].y;
     }
     const unsigned left = __shfl_up_sync(0xffffffffu, g1, 1);
     const unsigned right = __shfl_down_sync(0xffffffffu, g0, 1);
@@ -752,6 +766,11 @@ __device__ __forceinline__ void m3_pass(M3Stream<FMT, R>& st, unsigned char* __r
     r.g[0] = g0;
     r.g[1] = g1;
     if (k == kM3RPS - 1) st.release();
+  };
+  auto produce = [&](M3Row& r, int k) {
+    uint2 w[3];
+    fetch(k, w);
+    finish(r, k, w);
   };
 
   auto gauss_thres = [&](M3Row& r4, M3Row& r3, M3Row& r2, M3Row& r1, M3Row& r0, int gc) {
@@ -808,9 +827,17 @@ __device__ __forceinline__ void m3_pass(M3Stream<FMT, R>& st, unsigned char* __r
   // position (gc - y0 + 1) % 5, i.e. the step's position k in the unrolled
   // 5-step body (the body starts at gc = y0 - 1 + 5i).
   auto step = [&](M3Row& r4, M3Row& r3, M3Row& r2, M3Row& r1, M3Row& r0, int gc, int k) {
-    gauss_thres(r4, r3, r2, r1, r0, gc);
-    if (MODE != 0 && gc > y0) median(r4, r3, r2, gc - 1);
-    if (gc < gc_end) produce(r4, k);
+    if constexpr (R >= DF_M3_EARLY_MIN_R) {
+      uint2 w[3] = {};
+      if (gc < gc_end) fetch(k, w);
+      gauss_thres(r4, r3, r2, r1, r0, gc);
+      if (MODE != 0 && gc > y0) median(r4, r3, r2, gc - 1);
+      if (gc < gc_end) finish(r4, k, w);
+    } else {
+      gauss_thres(r4, r3, r2, r1, r0, gc);
+      if (MODE != 0 && gc > y0) median(r4, r3, r2, gc - 1);
+      if (gc < gc_end) produce(r4, k);
+    }
   };
 
 #pragma unroll
