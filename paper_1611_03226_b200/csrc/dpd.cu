@@ -184,12 +184,28 @@ __host__ __device__ constexpr int pad_index(int w) { return w + (w >> 3); }  // 
 template <int T>
 constexpr int dpd_min_blocks() { return T <= 16 ? 5 : 0; }
 
+// Warp-local windows for T <= DF_DPD_WARP_MAX_T: DPD-3 -1 % (1.165 vs 1.176
+// ms); T=32 would need 164 registers (3 CTAs/SM) and runs DPD-5 8 % slower
+// (profiles/r01_ab_dpd_variants.txt).
+#ifndef DF_DPD_WARP_MAX_T
+#define DF_DPD_WARP_MAX_T 16
+#endif
+// Window layout.  WL = 0: one CTA-wide window (thread tid owns positions
+// tid + m*THREADS), a __syncthreads per branch.  WL = 1: warp-local windows
+// -- warp w owns outputs [32V*w, 32V*(w+1)) of the tile and the 32V + T-1
+// window positions they read (lane l owns l + 32m; the T-1 positions before
+// the warp's first output are loaded and poly'd by both neighbouring warps),
+// so a branch needs only __syncwarp and warps never wait for each other.
 template <int T, int V, int THREADS>
 struct MainCfg {
+  static constexpr bool WL = T <= DF_DPD_WARP_MAX_T;
   static constexpr int S = THREADS * V;             // samples per tile
-  static constexpr int W = S + T - 1;               // window incl. history
+  static constexpr int NW = WL ? THREADS / 32 : 1;  // windows per CTA
+  static constexpr int OW = S / NW;                 // outputs per window
+  static constexpr int L = WL ? 32 : THREADS;       // threads sharing a window
+  static constexpr int W = OW + T - 1;              // window incl. history
   static constexpr int WP = pad_index(W) + 1;       // padded window length
-  static constexpr int M = (W + THREADS - 1) / THREADS;  // poly positions per thread
+  static constexpr int M = (W + L - 1) / L;         // poly positions per thread
 };
 
 // Fast-path state (see header): state = the carried FirState (read by
@@ -211,7 +227,7 @@ __global__ void __launch_bounds__(THREADS, dpd_min_blocks<T>()) dpd_main_kernel(
   constexpr int H1 = T - 1;
   constexpr int HS = H1 > 0 ? H1 : 1;
   __shared__ float2 taps_s[kBranches * T];
-  __shared__ float2 us[2][C::WP];
+  __shared__ float2 us_all[C::NW][2][C::WP];
   __shared__ float2 hist_s[FAST ? kBranches * HS : 1];  // fast path: this block's history per branch
   __shared__ int q_s[kBranches];
 
@@ -222,6 +238,10 @@ __global__ void __launch_bounds__(THREADS, dpd_min_blocks<T>()) dpd_main_kernel(
   float2* __restrict__ y = io_out(io);
 
   const int tid = threadIdx.x;
+  // Window-local thread index and the window's first output in the tile.
+  const int lt = C::WL ? (tid & 31) : tid;
+  const int wb = C::WL ? (tid >> 5) * C::OW : 0;
+  float2 (*us)[C::WP] = us_all[C::WL ? (tid >> 5) : 0];
   const unsigned t0 = tile * C::S;
   const int n = (int)min((unsigned)C::S, period - t0);  // valid outputs in this tile
   const size_t blk = (size_t)p * period;
@@ -233,15 +253,15 @@ __global__ void __launch_bounds__(THREADS, dpd_min_blocks<T>()) dpd_main_kernel(
 
   for (int i = tid; i < kBranches * T; i += THREADS) taps_s[i] = taps_g[i];
 
-  // Window position w in [0, W): sample index t0 - (T-1) + w of the block.
-  // Each thread owns positions w = tid + m*THREADS; keeps x, mag, scale.
+  // Window position w in [0, W): sample index t0 + wb - (T-1) + w of the
+  // block.  Each thread owns positions w = lt + m*L; keeps x, mag, scale.
   float xr[C::M], xi[C::M], mg[C::M], sc[C::M];
 #pragma unroll
   for (int m = 0; m < C::M; ++m) {
-    const int w = tid + m * THREADS;
-    const long long s = (long long)t0 - H1 + w;
+    const int w = lt + m * C::L;
+    const long long s = (long long)t0 + wb - H1 + w;
     float2 v = make_float2(0.f, 0.f);
-    if (w < n + H1 && s >= 0) v = __ldg(&x[blk + s]);
+    if (w < C::W && wb + w < n + H1 && s >= 0) v = __ldg(&x[blk + s]);
     xr[m] = v.x;
     xi[m] = v.y;
     mg[m] = __fsqrt_rn(__fadd_rn(__fmul_rn(v.x, v.x), __fmul_rn(v.y, v.y)));
@@ -293,12 +313,13 @@ __global__ void __launch_bounds__(THREADS, dpd_min_blocks<T>()) dpd_main_kernel(
     __syncthreads();
   }
   if (!fast && tile == 0) asm volatile("griddepcontrol.wait;" ::: "memory");  // history table from prep
+  if (C::WL) __syncthreads();  // taps_s (and hist_s) before the first branch
   int prev_b = 1;
   int buf = 0;
-  // Window slot of position tid + m*THREADS: pad_index(tid) + m * (THREADS
-  // + THREADS/8) (THREADS % 8 == 0), so the stores use immediate offsets.
-  static_assert(THREADS % 8 == 0, "window padding");
-  const int pt = pad_index(tid);
+  // Window slot of position lt + m*L: pad_index(lt) + m * (L + L/8)
+  // (L % 8 == 0), so the stores use immediate offsets.
+  static_assert(C::L % 8 == 0, "window padding");
+  const int pt = pad_index(lt);
   // Block-start tiles: this thread's history entry for branch b is
   // hb[(b - 1) * H1] (the prep kernel's table, u[-(tid+1)]).
   const bool has_hist = tile == 0 && tid < H1;
@@ -318,21 +339,24 @@ __global__ void __launch_bounds__(THREADS, dpd_min_blocks<T>()) dpd_main_kernel(
     float2* u = us[buf];
 #pragma unroll
     for (int m = 0; m < C::M; ++m) {
-      const int w = tid + m * THREADS;
+      const int w = lt + m * C::L;
       if (m < C::M - 1 || w < C::W) {
         // b == 1: sc = 1.0f and x * 1.0f == x exactly (no select needed)
-        u[pt + m * (THREADS + THREADS / 8)] = make_float2(__fmul_rn(xr[m], sc[m]), __fmul_rn(xi[m], sc[m]));
+        u[pt + m * (C::L + C::L / 8)] = make_float2(__fmul_rn(xr[m], sc[m]), __fmul_rn(xi[m], sc[m]));
       }
     }
     // History before the block start: the branch's frozen FIR state as
     // resolved by the prep kernel (u[-(j+1)] at window index H1-1-j).
     if (has_hist) u[hslot] = hb[(b - 1) * H1];
-    __syncthreads();
+    if (C::WL)
+      __syncwarp();
+    else
+      __syncthreads();
 
     // FIR over outputs o = tid*V + j (window index o + k' with k' = T-1-k).
     const float2* tb = taps_s + (b - 1) * T;
     float ar[V], ai[V], wr[V], wi[V];
-    const int o0 = tid * V;
+    const int o0 = lt * V;
 #pragma unroll
     for (int j = 0; j < V; ++j) {
       const float2 v = u[pad_index(o0 + H1 + j)];
@@ -374,13 +398,25 @@ __global__ void __launch_bounds__(THREADS, dpd_min_blocks<T>()) dpd_main_kernel(
   }
 
   // Stage through smem for coalesced stores (reuse the idle buffer).
-  __syncthreads();
+  if (C::WL)
+    __syncwarp();
+  else
+    __syncthreads();
   float2* st = us[buf];
 #pragma unroll
   for (int j = 0; j < V; ++j)
-    st[pad_index(tid * V + j)] = make_float2(__fadd_rn(outr[j], 0.0f), __fadd_rn(outi[j], 0.0f));
-  __syncthreads();
-  for (int o = tid; o < n; o += THREADS) y[blk + t0 + o] = st[pad_index(o)];
+    st[pad_index(lt * V + j)] = make_float2(__fadd_rn(outr[j], 0.0f), __fadd_rn(outi[j], 0.0f));
+  if (C::WL) {
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const int o = lt + 32 * i;
+      if (wb + o < n) y[blk + t0 + wb + o] = st[pad_index(o)];
+    }
+  } else {
+    __syncthreads();
+    for (int o = tid; o < n; o += THREADS) y[blk + t0 + o] = st[pad_index(o)];
+  }
   // The grid must not complete before the prep grid (which also advances
   // the FirState the next batch's prep reads).  Block-start tiles already
   // waited on it, and every batch has one, so no other CTA needs to: they
