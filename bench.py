@@ -216,15 +216,19 @@ def bench_motion_ours(args, p, rank, world, local):
             elif HALO != "ipc":
                 shard.exchange_tail(inp[(F - 1) * in_frame:], halos[0], rank, world)
         nstep[0] += 1
+        if rank == 0:
+            _lib.call("df_motion_set_prev_frame", actor.handle, None, sh)  # black initial token
+        if ev_k0 is not None:
+            ev_k0.record(stream)
         if rank > 0:
-            _lib.call("df_motion_set_prev_frame", actor.handle, C.c_void_p(halos[k].data_ptr()), sh)
+            # gauss(halo) is computed inside the firing (no separate pass)
+            _lib.call("df_motion_fire_halo", actor.handle, C.c_void_p(halos[k].data_ptr()),
+                      C.c_void_p(inp.data_ptr()), C.c_void_p(out.data_ptr()), F, sh)
             if pipe is not None:
                 pipe.release(k)
         else:
-            _lib.call("df_motion_set_prev_frame", actor.handle, None, sh)
-        if ev_k0 is not None:
-            ev_k0.record(stream)
-        _lib.call("df_motion_fire", actor.handle, C.c_void_p(inp.data_ptr()), C.c_void_p(out.data_ptr()), F, sh)
+            _lib.call("df_motion_fire", actor.handle, C.c_void_p(inp.data_ptr()), C.c_void_p(out.data_ptr()), F,
+                      sh)
         if ev_k1 is not None:
             ev_k1.record(stream)
 

@@ -227,6 +227,13 @@ int df_motion_set_prev_frame(df_motion* m, const void* frame_dev, void* stream);
  * and replaces the actor's internal delay token. */
 int df_motion_fire(df_motion* m, const void* in_dev, uint8_t* out_dev, uint32_t frames,
                    void* stream);
+/* Raw-buffer firing of a frame-range shard: like df_motion_set_prev_frame
+ * (m, halo_dev) followed by df_motion_fire, byte for byte, but gauss(halo)
+ * is computed inside the firing by the warps that start the shard (no
+ * separate gauss pass, no token round trip through HBM).  halo_dev is the
+ * previous shard's last input frame in the input format. */
+int df_motion_fire_halo(df_motion* m, const void* halo_dev, const void* in_dev, uint8_t* out_dev,
+                        uint32_t frames, void* stream);
 /* Channel-bound firing: `in` (token = one input frame, rate r), `delay`
  * (self-loop delay channel, token = W*H gauss bytes, rate 1, has_delay)
  * and `out` (token = W*H mask bytes, rate r).  Regions and the Fig. 2

@@ -123,6 +123,7 @@ _SIGS = {
     "df_motion_destroy": (_i, [_vp]),
     "df_motion_set_prev_frame": (_i, [_vp, _vp, _vp]),
     "df_motion_fire": (_i, [_vp, _vp, _vp, _u32, _vp]),
+    "df_motion_fire_halo": (_i, [_vp, _vp, _vp, _vp, _u32, _vp]),
     "df_motion_fire_channels": (_i, [_vp, _vp, _vp, _vp, _vp]),
     "df_motion_run_host": (_i, [_vp, _vp, _vp, _u64, _u32, _vp]),
     "df_motion_gauss5x5": (_i, [_vp, _vp, C.c_uint, C.c_uint, _vp]),

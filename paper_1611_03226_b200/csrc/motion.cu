@@ -65,6 +65,7 @@ struct MotionIO {
   const unsigned char* prev;    // delay token in (gauss frame)
   unsigned char* next;          // delay token out (gauss frame)
   unsigned char* next_copy;     // Fig. 2 phase-2 duplicate (slot 0) or null
+  const unsigned char* halo;    // raw mode: previous input frame replacing the delay token, or null
   DevChan in_ch, out_ch, delay_ch;
   int channel_mode;
 };
@@ -670,6 +671,8 @@ struct M3Stream {
   static_assert(m3_valid_r<R>(), "band height");
   static constexpr int GPP = (R + 6) / kM3RPS;  // groups per frame pass
   const CUtensorMap* map;
+  const CUtensorMap* hmap;  // inline halo: pass 0 reads frame 0 of this map
+  bool hfirst;
   unsigned ring;      // smem address of this warp's ring
   unsigned bars;      // smem address of this warp's kM3Stages mbarriers
   unsigned g;         // group being consumed
@@ -686,7 +689,10 @@ struct M3Stream {
     const unsigned pass = gi / GPP;
     const int row = y0 - 3 + (int)(gi % GPP) * kM3RPS;
     mbar_expect_tx(bars + 8 * s, kM3RPS * m3_row_bytes<FMT>());
-    tma_load_2d(ring + s * m3_stage_bytes<FMT>(), map, c0, (fs + (int)pass) * H + row, bars + 8 * s);
+    if (hfirst && pass == 0)
+      tma_load_2d(ring + s * m3_stage_bytes<FMT>(), hmap, c0, row, bars + 8 * s);
+    else
+      tma_load_2d(ring + s * m3_stage_bytes<FMT>(), map, c0, (fs + (int)pass) * H + row, bars + 8 * s);
   }
   __device__ __forceinline__ void acquire() {
     mbar_wait(bars + 8 * stage, phase);
@@ -878,14 +884,14 @@ __device__ __forceinline__ void m3_walk(M3Stream<FMT, R>& st, const unsigned cha
   const size_t frame_px = (size_t)g.W * g.H;
   unsigned gm[2], mm[2];
   column_masks(x, g.W, gm, mm);
-  if (f_begin == 0) {
+  if (f_begin == 0 && !st.hfirst) {
     // Delay token: gauss of the previous firing's last frame -> TMEM.
     for (int r = 0; r < R + 2; ++r) {
       unsigned a0, a1;
       load_bytes8<true>(prev_tok, y0 - 1 + r, x, g.W, g.H, a0, a1);
       tmem_st2(tmem + 2u * r, a0, a1);
     }
-  } else {
+  } else {  // gauss(f_begin - 1): the previous frame, or the inline halo frame
     m3_pass<FMT, R, 0, INT>(st, nullptr, nullptr, nullptr, tmem, g, y0, x, lane, gm, mm);
   }
   const int f_last = (f_end == g.frames) ? f_end - 1 : f_end;
@@ -897,6 +903,7 @@ __device__ __forceinline__ void m3_walk(M3Stream<FMT, R>& st, const unsigned cha
 
 template <int FMT, int R>
 __global__ void __launch_bounds__(32 * kM3Warps, 4) motion_m3_kernel(const __grid_constant__ CUtensorMap map,
+                                                                   const __grid_constant__ CUtensorMap hmap,
                                                                    MotionIO io, MotionGeom g,
                                                                    unsigned* done_counter) {
   extern __shared__ __align__(128) unsigned char m3_smem[];
@@ -920,6 +927,10 @@ __global__ void __launch_bounds__(32 * kM3Warps, 4) motion_m3_kernel(const __gri
   }
   M3Stream<FMT, R> st;
   st.map = &map;
+  st.hmap = &hmap;
+  // Inline halo (raw mode): the first chunk warms up on the halo frame
+  // instead of loading a delay token -- gauss(halo) never goes through HBM.
+  st.hfirst = io.halo != nullptr && f_begin == 0;
   st.ring = smem_u32(m3_smem + warp * m3_ring_bytes<FMT>());
   st.bars = smem_u32(m3_smem + kM3Warps * m3_ring_bytes<FMT>() + warp * kM3Stages * 8);
   st.g = 0;
@@ -945,7 +956,7 @@ __global__ void __launch_bounds__(32 * kM3Warps, 4) motion_m3_kernel(const __gri
     next_copy = chan_write_wraps(io.delay_ch) ? io.delay_ch.storage : nullptr;
   }
   st.lane = lane;
-  const int f_first = f_begin > 0 ? f_begin - 1 : f_begin;  // warm-up frame of a later chunk
+  const int f_first = (f_begin > 0 || st.hfirst) ? f_begin - 1 : f_begin;  // warm-up frame
   st.fs = base + f_first;
   const int passes = f_begin < f_end ? f_end - f_first : 0;
   st.groups = (unsigned)passes * M3Stream<FMT, R>::GPP;
@@ -1198,6 +1209,14 @@ int launch_m3(df_motion* m, const MotionIO& io, int frames, cudaStream_t s) {
                                      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   DF_REQUIRE(cr == CUDA_SUCCESS, DF_ECUDA, "motion: cuTensorMapEncodeTiled failed (%d)", (int)cr);
+  CUtensorMap hmap = map;
+  if (io.halo) {  // one frame, same box
+    const cuuint64_t hdims[2] = {(cuuint64_t)m->W * FMT / 4, (cuuint64_t)m->H};
+    cr = tensor_map_encoder()(&hmap, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<unsigned char*>(io.halo), hdims,
+                              strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    DF_REQUIRE(cr == CUDA_SUCCESS, DF_ECUDA, "motion: cuTensorMapEncodeTiled (halo) failed (%d)", (int)cr);
+  }
   const int tiles = (m->W + kOutPxPerWarp - 1) / kOutPxPerWarp;
   dim3 grid(tiles, best.bands, (best.chunks + kM3Warps - 1) / kM3Warps);
   if (getenv("DF_DEBUG"))
@@ -1205,11 +1224,11 @@ int launch_m3(df_motion* m, const MotionIO& io, int frames, cudaStream_t s) {
             kM3Heights[best.ri], m->m3_resident[best.ri], grid.x, grid.y, grid.z, g.chunk, m3_smem_bytes<FMT>());
   const size_t smem = m3_smem_bytes<FMT>();
   if (best.ri == 0)
-    motion_m3_kernel<FMT, kM3Heights[0]><<<grid, 32 * kM3Warps, smem, s>>>(map, io, g, m->scratch);
+    motion_m3_kernel<FMT, kM3Heights[0]><<<grid, 32 * kM3Warps, smem, s>>>(map, hmap, io, g, m->scratch);
   else if (best.ri == 1)
-    motion_m3_kernel<FMT, kM3Heights[1]><<<grid, 32 * kM3Warps, smem, s>>>(map, io, g, m->scratch);
+    motion_m3_kernel<FMT, kM3Heights[1]><<<grid, 32 * kM3Warps, smem, s>>>(map, hmap, io, g, m->scratch);
   else
-    motion_m3_kernel<FMT, kM3Heights[2]><<<grid, 32 * kM3Warps, smem, s>>>(map, io, g, m->scratch);
+    motion_m3_kernel<FMT, kM3Heights[2]><<<grid, 32 * kM3Warps, smem, s>>>(map, hmap, io, g, m->scratch);
   return after_launch("motion_m3_kernel");
 }
 
@@ -1340,6 +1359,30 @@ int df_motion_fire(df_motion* m, const void* in_dev, uint8_t* out_dev, uint32_t 
   io.next = m->tok[m->cur ^ 1];
   io.next_copy = nullptr;
   io.channel_mode = 0;
+  DF_TRY(launch_motion(m, io, (int)frames, as_stream(stream)));
+  m->cur ^= 1;
+  return DF_OK;
+}
+
+int df_motion_fire_halo(df_motion* m, const void* halo_dev, const void* in_dev, uint8_t* out_dev,
+                        uint32_t frames, void* stream) {
+  DF_REQUIRE(m, DF_EINVAL, "df_motion_fire_halo: null actor");
+  if (frames == 0) return DF_OK;
+  DF_REQUIRE(halo_dev && in_dev && out_dev, DF_EINVAL, "df_motion_fire_halo: null buffer");
+  DF_REQUIRE(frames <= (1u << 30), DF_EINVAL, "df_motion_fire_halo: too many frames");
+  DF_CHECK_CUDA(cudaSetDevice(m->device));
+  MotionIO io{};
+  io.in = (const unsigned char*)in_dev;
+  io.out = out_dev;
+  io.prev = m->tok[m->cur];
+  io.next = m->tok[m->cur ^ 1];
+  io.halo = (const unsigned char*)halo_dev;
+  const bool halo_ok = (reinterpret_cast<uintptr_t>(halo_dev) & 15) == 0;
+  if (!m3_eligible(m, io, (int)frames) || !halo_ok) {
+    // Register-prefetch kernel: the halo becomes the delay token first.
+    DF_TRY(df_motion_set_prev_frame(m, halo_dev, stream));
+    return df_motion_fire(m, in_dev, out_dev, frames, stream);
+  }
   DF_TRY(launch_motion(m, io, (int)frames, as_stream(stream)));
   m->cur ^= 1;
   return DF_OK;

@@ -39,6 +39,13 @@ class MotionActor:
         call("df_motion_fire", self.handle, inp.at(in_offset), out.at(out_offset), int(frames),
              stream.handle if stream else None)
 
+    def fire_halo(self, halo: Buffer, inp: Buffer, out: Buffer, frames: int, stream: Stream | None = None,
+                  halo_offset: int = 0, in_offset: int = 0, out_offset: int = 0):
+        """Shard firing: `halo` (the previous shard's last input frame) stands
+        in for the delay token; gauss(halo) is computed inside the firing."""
+        call("df_motion_fire_halo", self.handle, halo.at(halo_offset), inp.at(in_offset), out.at(out_offset),
+             int(frames), stream.handle if stream else None)
+
     @property
     def kernel_name(self) -> str:
         """The kernel a firing launches (for 16-byte aligned inputs)."""

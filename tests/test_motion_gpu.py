@@ -176,6 +176,26 @@ def test_frame_range_shard_with_halo(gpu):
         assert_frames_equal(got, full[f0 * fsz: f1 * fsz], w, h)
 
 
+@pytest.mark.parametrize("w,h,n", [(96, 48, 12), (1280, 72, 9), (160, 130, 40), (44, 30, 6), (250, 61, 17)])
+def test_fire_halo_equals_shard_of_full_run(gpu, w, h, n):
+    """df_motion_fire_halo (gauss of the halo frame computed in-kernel by the
+    shard's first temporal chunk) == the same shard of the full run, for M3
+    widths (96, 1280, 160: W*3 % 16 == 0) and fallback widths (44, 250)."""
+    from paper_1611_03226_b200 import device, motion
+    rgb = O.synth_bytes(n * w * h * 3, 1000 + w)
+    full = O.motion_rgb(rgb, w, h)
+    fb = w * h * 3
+    f0, f1 = n // 3, n - 2
+    a = motion.MotionActor(w, h, motion.RGB, 32)
+    inp = device.Buffer.from_array(rgb[f0 * fb:])
+    halo = device.Buffer.from_array(rgb[(f0 - 1) * fb:f0 * fb])
+    out = device.Buffer((n - f0) * w * h)
+    a.fire_halo(halo, inp, out, f1 - f0)
+    # ... and the delay token it leaves carries into the next firing
+    a.fire(inp, out, n - f1, in_offset=(f1 - f0) * fb, out_offset=(f1 - f0) * w * h)
+    assert_frames_equal(out.download(np.uint8), full[f0 * w * h:], w, h)
+
+
 def test_first_frame_against_black(gpu):
     # proj/tests/test_motion.cpp:183-192
     f = np.full(8 * 8, 200, np.uint8)

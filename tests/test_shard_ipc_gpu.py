@@ -45,9 +45,11 @@ def _motion_worker(rank, world, port, q):
             prev_frames = shard.frame_shards(n, world)[rank - 1]
             last = (prev_frames[1] - prev_frames[0] - 1) * fb
             _lib.call("df_halo_copy", 0, halo.ptr, peer.device, C.c_void_p(peer.ptr + last), fb, None)
-            _lib.call("df_motion_set_prev_frame", actor.handle, halo.ptr, None)
         out = device.Buffer((f1 - f0) * w * h)
-        _lib.call("df_motion_fire", actor.handle, mine.ptr, out.ptr, f1 - f0, None)
+        if rank > 0:
+            actor.fire_halo(halo, mine, out, f1 - f0)
+        else:
+            actor.fire(mine, out, f1 - f0)
         q.put((rank, out.download(np.uint8)))
         peer.close()
         dist.barrier()
