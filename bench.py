@@ -393,25 +393,25 @@ def bench_dpd_ours(args, p, rank, world, local):
     for b in range(1, 11):
         hb = shard.dpd_halo_block(sched, blocks, b)  # last active block of this rank (local index)
         tail_src.append(hb)
-    peer = pipe = None
+    peer = None
     if world > 1:
         torch.cuda.synchronize()
         dist.barrier()  # every shard is filled before a neighbour maps it
         if HALO == "ipc":
             peer = shard.PeerBuffer(x.data_ptr(), local, rank, world)
-            if rank > 0:
-                pipe = HaloPipe(torch, stream, local, peer.device)
-    nstep = [0]
+    # IPC: the firing reads each branch's halo tail straight from the
+    # neighbour's mapped shard over NVLink (df_dpd_fire_halo) -- no copy, no
+    # extra launch; only the block-start tiles that need a tail touch it.
+    tail_ptrs = None
+    if peer is not None and rank > 0:
+        tail_ptrs = (C.c_void_p * 10)(*[C.c_void_p(peer.ptr + 8 * ((hb + 1) * period - H1)) if hb is not None
+                                        else None for hb in tail_src])
 
     def step(ev0=None, ev1=None):
         sh = C.c_void_p(torch.cuda.current_stream().cuda_stream)  # the capture stream inside a graph
-        if world > 1:
+        if world > 1 and tail_ptrs is None:
             k, got = 0, rank > 0
-            if pipe is not None:
-                k = nstep[0] % 2
-                pipe.pull(nstep[0], [(halos[k].data_ptr() + 8 * H1 * b, peer.ptr + 8 * ((hb + 1) * period - H1),
-                                      8 * H1) for b, hb in enumerate(tail_src) if hb is not None])
-            elif HALO != "ipc":
+            if HALO != "ipc":
                 for b, hb in enumerate(tail_src):
                     if hb is not None:
                         a0 = 2 * ((hb + 1) * period - H1)
@@ -421,13 +421,14 @@ def bench_dpd_ours(args, p, rank, world, local):
                 for b in range(10):
                     _lib.call("df_dpd_set_history", actor.handle, C.c_void_p(halos[k].data_ptr() + 8 * H1 * b), H1,
                               1 << b, sh)
-                if pipe is not None:
-                    pipe.release(k)
-        nstep[0] += 1
         if ev0 is not None:
             ev0.record(stream)
-        _lib.call("df_dpd_fire", actor.handle, C.c_void_p(ctrl.data_ptr()), C.c_void_p(x.data_ptr()),
-                  C.c_void_p(y.data_ptr()), blocks, sh)
+        if tail_ptrs is not None:
+            _lib.call("df_dpd_fire_halo", actor.handle, tail_ptrs, C.c_void_p(ctrl.data_ptr()),
+                      C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), blocks, sh)
+        else:
+            _lib.call("df_dpd_fire", actor.handle, C.c_void_p(ctrl.data_ptr()), C.c_void_p(x.data_ptr()),
+                      C.c_void_p(y.data_ptr()), blocks, sh)
         if ev1 is not None:
             ev1.record(stream)
 
@@ -490,7 +491,7 @@ def bench_dpd_ours(args, p, rank, world, local):
         "config": {"workload": p["label"], "samples_per_gpu": N, "period": period, "taps_per_branch": T,
                    "schedule": p["sched"],
                    "parallelism": f"block-range shards x{world}, per-branch FIR-history halo via "
-                                  + ("NVLink peer copies (CUDA IPC), overlapped" if HALO == "ipc" else "NCCL P2P"),
+                                  + ("in-kernel NVLink peer reads (CUDA IPC)" if HALO == "ipc" else "NCCL P2P"),
                    "l2": f"in+out {16 * N / 1e6:.0f} MB per GPU"},
         "e2e": {"value": round(world * N / e2e_s / 1e6, 1), "unit": "Msamples/s",
                 "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * N,

@@ -184,7 +184,17 @@ int df_dpd_set_history(df_dpd* dpd, const float* raw_dev, uint32_t count, uint32
  * sequential firings of the reference's dynamic part. */
 int df_dpd_fire(df_dpd* dpd, const uint32_t* ctrl_dev, const float* in_dev, float* out_dev,
                 uint64_t blocks, void* stream);
-/* Channel-bound firing: consumes `firings` control tokens from `ctrl`
+/* Raw-buffer firing of a block-range shard with its FIR-history halo:
+ * halo_tails[b-1] is a device pointer -- local, or a peer pointer into the
+ * previous shard's input on another GPU (df_ipc_open_handle) -- to the
+ * last T-1 raw interleaved samples, oldest first, of branch b's last
+ * active block before this shard, or NULL (branch b keeps its carried
+ * history).  Equivalent to df_dpd_set_history(dpd, halo_tails[b-1], T-1,
+ * 1 << (b-1)) for each non-NULL b followed by df_dpd_fire; on the fast path
+ * the tiles that need a halo read it directly (over NVLink for a peer
+ * pointer) inside the firing. */
+int df_dpd_fire_halo(df_dpd* dpd, const float* const* halo_tails, const uint32_t* ctrl_dev,
+                     const float* in_dev, float* out_dev, uint64_t blocks, void* stream);/* Channel-bound firing: consumes `firings` control tokens from `ctrl`
  * (token 4 B, rate 1) and one block token per firing from `in`
  * (token = period*8 B); produces one block token per firing into `out`.
  * All three channels must have token_rate == firings (a batched GPU actor

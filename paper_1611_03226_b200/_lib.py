@@ -116,6 +116,7 @@ _SIGS = {
     "df_dpd_error": (_i, [_vp]),
     "df_dpd_set_history": (_i, [_vp, _vp, _u32, _u32, _vp]),
     "df_dpd_fire": (_i, [_vp, _vp, _vp, _vp, _u64, _vp]),
+    "df_dpd_fire_halo": (_i, [_vp, _vp, _vp, _vp, _vp, _u64, _vp]),
     "df_dpd_fire_channels": (_i, [_vp, _vp, _vp, _vp, _u32, _vp]),
     "df_dpd_config_tokens": (_i, [_i, _vp, _sz, _u64, _u64, _vp, _vp]),
     "df_dpd_run_host": (_i, [_vp, _vp, _vp, _u64, _vp, _sz, _u64, _vp]),

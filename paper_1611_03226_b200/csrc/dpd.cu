@@ -212,10 +212,26 @@ struct MainCfg {
 // block-start tiles with no earlier active block, advanced in place by the
 // grid's last CTA); last1[b] = 1 + last active block of branch b+1 in the
 // batch (0: none), reset by the last CTA.
+// htail[b] (optional, df_dpd_fire_halo): the last T-1 raw samples,
+// oldest first, of branch b+1's last active block before the batch --
+// typically a peer pointer into the previous shard's input on another GPU
+// (CUDA IPC, read over NVLink by the few tiles that need it).  It replaces
+// the carried state for that branch, as df_dpd_set_history would.
 struct FastState {
   float2* state;
   int* last1;
+  const float2* htail[kBranches];
 };
+
+// History sample u[-(j+1)] of branch bi+1 with no active block earlier in
+// the batch: from the halo tail if given, else the carried FirState.
+__device__ __forceinline__ float2 carried_history(const FastState& fs, int bi, int j, int H1) {
+  if (const float2* t = fs.htail[bi]) {
+    const float2 v = t[H1 - 1 - j];
+    return poly_sample(v.x, v.y, bi + 1);
+  }
+  return fs.state[bi * (kMaxTaps - 1) + j];
+}
 
 template <int T, int V, int THREADS, bool FAST>
 __global__ void __launch_bounds__(THREADS, dpd_min_blocks<T>()) dpd_main_kernel(DpdIO io, const float2* __restrict__ taps_g,
@@ -307,7 +323,7 @@ __global__ void __launch_bounds__(THREADS, dpd_min_blocks<T>()) dpd_main_kernel(
         const float2 v = __ldg(&x[(size_t)q * period + (period - 1 - j)]);
         hist_s[it] = poly_sample(v.x, v.y, bi + 1);
       } else {
-        hist_s[it] = fs.state[bi * (kMaxTaps - 1) + j];
+        hist_s[it] = carried_history(fs, bi, j, H1);
       }
     }
     __syncthreads();
@@ -443,6 +459,8 @@ __global__ void __launch_bounds__(THREADS, dpd_min_blocks<T>()) dpd_main_kernel(
         if (q >= 0) {
           const float2 v = x[(size_t)q * period + (period - 1 - j)];
           fs.state[bi * (kMaxTaps - 1) + j] = poly_sample(v.x, v.y, bi + 1);
+        } else if (fs.htail[bi]) {  // gated off all batch: the halo becomes the state
+          fs.state[bi * (kMaxTaps - 1) + j] = carried_history(fs, bi, j, H1);
         }
       }
       __syncthreads();
@@ -596,19 +614,27 @@ int ensure_hist(df_dpd* d, unsigned long long K) {
   return DF_OK;
 }
 
-int launch_dpd(df_dpd* d, const DpdIO& io, unsigned long long K, cudaStream_t s) {
+bool dpd_fast_path(const df_dpd* d) {
+  return ((d->T == 10 && (DF_DPD_FAST & 1)) || (d->T == 32 && (DF_DPD_FAST & 2))) && d->period >= d->T - 1;
+}
+
+// htail: optional per-branch halo tails (df_dpd_fire_halo; fast path only).
+int launch_dpd(df_dpd* d, const DpdIO& io, unsigned long long K, cudaStream_t s,
+               const float2* const* htail = nullptr) {
   if (K == 0) return DF_OK;
   DF_REQUIRE(K <= 0x7fffffffull / 2, DF_EINVAL, "dpd: batch of %llu blocks too large", K);
   DF_TRY(ensure_hist(d, K));
   unsigned* err = d->scratch;
   unsigned* done = d->scratch + 1;
   // Fast path (see the header): T in {10, 32} and blocks at least T-1 long.
-  const bool fast = ((d->T == 10 && (DF_DPD_FAST & 1)) || (d->T == 32 && (DF_DPD_FAST & 2))) && d->period >= d->T - 1;
+  const bool fast = dpd_fast_path(d);
   // (FAST is a template parameter: the prep-path kernel keeps its own code.)
   FastState fs{};
   if (fast) {
     fs.state = d->state;
     fs.last1 = reinterpret_cast<int*>(d->scratch + 4);
+    if (htail)
+      for (int b = 0; b < kBranches; ++b) fs.htail[b] = htail[b];
   }
   if (d->T > 1 && !fast) {
     dpd_prep_kernel<<<kBranches, 1024, 0, s>>>(io, d->state, d->state, d->hist, d->act, K, d->period,
@@ -649,6 +675,9 @@ int launch_dpd(df_dpd* d, const DpdIO& io, unsigned long long K, cudaStream_t s)
                              : cudaLaunchKernelEx(&lc, dpd_main_kernel<32, kV, kThreads, false>, sub, tp, hist, d->period, tiles, err, done, fs));
       DF_CHECK_CUDA(le);
       DF_TRY(after_launch("dpd_main_kernel"));
+      // Later sub-launches continue from the state this one advanced (which
+      // already holds the halo of branches it never saw active).
+      for (int b = 0; b < kBranches; ++b) fs.htail[b] = nullptr;
     }
   } else {
     for (unsigned long long base = 0; base < K; base += 65535) {
@@ -783,6 +812,29 @@ int df_dpd_fire(df_dpd* d, const uint32_t* ctrl_dev, const float* in_dev, float*
   io.out = reinterpret_cast<float2*>(out_dev);
   io.channel_mode = 0;
   return launch_dpd(d, io, blocks, as_stream(stream));
+}
+
+int df_dpd_fire_halo(df_dpd* d, const float* const* halo_tails, const uint32_t* ctrl_dev, const float* in_dev,
+                     float* out_dev, uint64_t blocks, void* stream) {
+  DF_REQUIRE(d, DF_EINVAL, "df_dpd_fire_halo: null actor");
+  if (blocks == 0) return DF_OK;
+  DF_REQUIRE(halo_tails && ctrl_dev && in_dev && out_dev, DF_EINVAL, "df_dpd_fire_halo: null argument");
+  DF_REQUIRE(in_dev != out_dev, DF_EINVAL, "df_dpd_fire_halo: in-place firing is not supported");
+  DF_CHECK_CUDA(cudaSetDevice(d->device));
+  if (d->T <= 1) return df_dpd_fire(d, ctrl_dev, in_dev, out_dev, blocks, stream);
+  if (!dpd_fast_path(d)) {  // prep path: set the histories, then fire
+    for (int b = 0; b < kBranches; ++b)
+      if (halo_tails[b]) DF_TRY(df_dpd_set_history(d, halo_tails[b], d->T - 1, 1u << b, stream));
+    return df_dpd_fire(d, ctrl_dev, in_dev, out_dev, blocks, stream);
+  }
+  const float2* ht[kBranches];
+  for (int b = 0; b < kBranches; ++b) ht[b] = reinterpret_cast<const float2*>(halo_tails[b]);
+  DpdIO io{};
+  io.ctrl = ctrl_dev;
+  io.in = reinterpret_cast<const float2*>(in_dev);
+  io.out = reinterpret_cast<float2*>(out_dev);
+  io.channel_mode = 0;
+  return launch_dpd(d, io, blocks, as_stream(stream), ht);
 }
 
 int df_dpd_fire_channels(df_dpd* d, df_channel* ctrl, df_channel* in, df_channel* out,

@@ -79,6 +79,15 @@ class DpdActor:
         call("df_dpd_fire", self.handle, ctrl.at(ctrl_offset), inp.at(in_offset), out.at(out_offset),
              int(blocks), stream.handle if stream else None)
 
+    def fire_halo(self, halo_tails, ctrl: Buffer, inp: Buffer, out: Buffer, blocks: int,
+                  stream: Stream | None = None, ctrl_offset: int = 0, in_offset: int = 0, out_offset: int = 0):
+        """Shard firing: halo_tails[b-1] = device address (int, local or an
+        IPC peer pointer) of branch b's last T-1 raw samples before the
+        shard, or None to keep the carried history."""
+        arr = (C.c_void_p * 10)(*[C.c_void_p(t) if t else None for t in halo_tails])
+        call("df_dpd_fire_halo", self.handle, arr, ctrl.at(ctrl_offset), inp.at(in_offset), out.at(out_offset),
+             int(blocks), stream.handle if stream else None)
+
     def fire_channels(self, ctrl_ch, in_ch, out_ch, firings: int, stream: Stream | None = None):
         call("df_dpd_fire_channels", self.handle, ctrl_ch.handle, in_ch.handle, out_ch.handle,
              int(firings), stream.handle if stream else None)

@@ -114,6 +114,47 @@ def test_long_gated_off_stretches(gpu, T, chunk):
     assert_parity(run_gpu(x, taps, sched, period, chunk_blocks=chunk), O.dpd(x, taps, sched, period))
 
 
+def _branch_tails(x, sched, period, first_block, T):
+    """Per branch: the last T-1 raw samples of its active stream before
+    `first_block` (None if it has fewer than T-1 -- then part of the state
+    would come from zeros, which set_history cannot express; not used)."""
+    xs = x.reshape(-1, period, 2)
+    tails = []
+    for b in range(1, 11):
+        act = [p for p in range(first_block) if (int(sched[p % len(sched)]) >> (b - 1)) & 1]
+        stream = xs[act].reshape(-1, 2) if act else np.zeros((0, 2), np.float32)
+        tails.append(np.ascontiguousarray(stream[-(T - 1):]) if len(stream) >= T - 1 else None)
+    return tails
+
+
+@pytest.mark.parametrize("T,period", [(10, 256), (10, 64), (32, 256), (10, 4)])
+def test_fire_halo_shard_equals_full_run(gpu, T, period):
+    """df_dpd_fire_halo on a block-range shard, with per-branch halo tails of
+    the stream before it, equals the shard of the full run (fast path: T=10
+    with blocks >= T-1; prep path: T=32 and 4-sample blocks)."""
+    from paper_1611_03226_b200 import device, dpd
+    blocks = 40
+    x = O.synth_samples(period * blocks, 77 + T + period)
+    taps = O.random_taps(78, T)
+    sched = np.array([0x3FF, 0x001, 0x2A5, 0x0F0, 0x100, 0x3FF, 0x003, 0x200, 0x3FF], np.uint16)
+    want = O.dpd(x, taps, sched, period)
+    b0 = 23
+    tails = _branch_tails(x, sched, period, b0, T)
+    bufs = [device.Buffer.from_array(t) if t is not None else None for t in tails]
+    a = dpd.DpdActor(period, taps)
+    nb = blocks - b0
+    ctrl = device.Buffer(4 * nb)
+    dpd.config_tokens(sched, b0, nb, ctrl)
+    inp = device.Buffer.from_array(x[2 * period * b0:])
+    out = device.Buffer(8 * period * nb)
+    half = nb // 2  # two firings: the second continues from the state the first left
+    a.fire_halo([bb.ptr.value if bb is not None else None for bb in bufs], ctrl, inp, out, half)
+    a.fire(ctrl, inp, out, nb - half, ctrl_offset=4 * half, in_offset=8 * period * half,
+           out_offset=8 * period * half)
+    a.check()
+    assert_parity(out.download(np.float32), want[2 * period * b0:])
+
+
 def test_gating_invariance_acceptance9(gpu):
     # proj/tests/acceptance.cpp:398-450: branch 7 toggled; inactive periods
     # must be bit-identical when its taps change.

@@ -1,7 +1,9 @@
 """GPU, world size 2 (two processes on cuda:0, gloo for setup only): the
 N>1 transport of bench.py -- each rank exports its shard buffer once (CUDA
-IPC), the next rank maps it and pulls its halo with a copy-engine peer copy
-(df_halo_copy), then fires its shard through the C ABI.  The concatenated
+IPC), the next rank maps it; motion pulls its one-frame halo with a
+copy-engine peer copy (df_halo_copy) and fires with df_motion_fire_halo,
+DPD fires with df_dpd_fire_halo reading the per-branch tails straight from
+the neighbour's mapped shard.  The concatenated
 shard outputs must equal the oracle on the unsharded stream, byte for byte
 (motion: frame-range shards, one-frame halo) and bit for bit (DPD:
 block-range shards, per-branch FIR-history halos, dynamic schedule)."""
@@ -74,19 +76,20 @@ def _dpd_worker(rank, world, port, q):
         dist.barrier()
         peer = shard.PeerBuffer(mine.ptr.value, 0, rank, world)
         actor = dpd.DpdActor(period, taps)
+        out = device.Buffer(8 * (s1 - s0))
         if rank > 0:
             # Per branch: the tail of its last active block before this shard
-            # (on the previous rank here: every branch fires in its range).
+            # (on the previous rank here: every branch fires in its range),
+            # read by the firing straight from the neighbour's mapped shard.
             p0 = shard.block_shards(period * blocks, period, world)[rank - 1][0] // period
-            halo = device.Buffer(8 * (T - 1))
+            tails = []
             for b in range(1, 11):
                 hb = shard.dpd_halo_block(sched, b0, b)
                 assert hb is not None and hb >= p0
-                src = peer.ptr + 8 * ((hb - p0 + 1) * period - (T - 1))
-                _lib.call("df_halo_copy", 0, halo.ptr, peer.device, C.c_void_p(src), 8 * (T - 1), None)
-                _lib.call("df_dpd_set_history", actor.handle, halo.ptr, T - 1, 1 << (b - 1), None)
-        out = device.Buffer(8 * (s1 - s0))
-        actor.fire(ctrl, mine, out, nb)
+                tails.append(peer.ptr + 8 * ((hb - p0 + 1) * period - (T - 1)))
+            actor.fire_halo(tails, ctrl, mine, out, nb)
+        else:
+            actor.fire(ctrl, mine, out, nb)
         actor.check()
         q.put((rank, out.download(np.float32)))
         peer.close()
