@@ -225,15 +225,20 @@ struct FastState {
 
 // History sample u[-(j+1)] of branch bi+1 with no active block earlier in
 // the batch: from the halo tail if given, else the carried FirState.
+template <bool HALO>
 __device__ __forceinline__ float2 carried_history(const FastState& fs, int bi, int j, int H1) {
-  if (const float2* t = fs.htail[bi]) {
+  const float2* t = HALO ? fs.htail[bi] : nullptr;
+  if (t) {
     const float2 v = t[H1 - 1 - j];
     return poly_sample(v.x, v.y, bi + 1);
   }
   return fs.state[bi * (kMaxTaps - 1) + j];
 }
 
-template <int T, int V, int THREADS, bool FAST>
+// HALO: the firing takes per-branch halo tails (df_dpd_fire_halo); a
+// separate instantiation, so plain firings keep their register allocation
+// (with the tails compiled in, DPD-1 ran 7 % slower).
+template <int T, int V, int THREADS, bool FAST, bool HALO>
 __global__ void __launch_bounds__(THREADS, dpd_min_blocks<T>()) dpd_main_kernel(DpdIO io, const float2* __restrict__ taps_g,
                                                             const float2* __restrict__ hist,
                                                             unsigned period, unsigned tiles_per_block,
@@ -323,7 +328,7 @@ __global__ void __launch_bounds__(THREADS, dpd_min_blocks<T>()) dpd_main_kernel(
         const float2 v = __ldg(&x[(size_t)q * period + (period - 1 - j)]);
         hist_s[it] = poly_sample(v.x, v.y, bi + 1);
       } else {
-        hist_s[it] = carried_history(fs, bi, j, H1);
+        hist_s[it] = carried_history<HALO>(fs, bi, j, H1);
       }
     }
     __syncthreads();
@@ -459,8 +464,8 @@ __global__ void __launch_bounds__(THREADS, dpd_min_blocks<T>()) dpd_main_kernel(
         if (q >= 0) {
           const float2 v = x[(size_t)q * period + (period - 1 - j)];
           fs.state[bi * (kMaxTaps - 1) + j] = poly_sample(v.x, v.y, bi + 1);
-        } else if (fs.htail[bi]) {  // gated off all batch: the halo becomes the state
-          fs.state[bi * (kMaxTaps - 1) + j] = carried_history(fs, bi, j, H1);
+        } else if (HALO && fs.htail[bi]) {  // gated off all batch: the halo becomes the state
+          fs.state[bi * (kMaxTaps - 1) + j] = carried_history<HALO>(fs, bi, j, H1);
         }
       }
       __syncthreads();
@@ -668,11 +673,16 @@ int launch_dpd(df_dpd* d, const DpdIO& io, unsigned long long K, cudaStream_t s,
       lc.attrs = attr;
       lc.numAttrs = fast ? 0 : 1;  // PDL only behind the prep kernel
       const float2* tp = d->taps;
-      cudaError_t le =
-          d->T == 10 ? (fast ? cudaLaunchKernelEx(&lc, dpd_main_kernel<10, kV, kThreads, true>, sub, tp, hist, d->period, tiles, err, done, fs)
-                             : cudaLaunchKernelEx(&lc, dpd_main_kernel<10, kV, kThreads, false>, sub, tp, hist, d->period, tiles, err, done, fs))
-                     : (fast ? cudaLaunchKernelEx(&lc, dpd_main_kernel<32, kV, kThreads, true>, sub, tp, hist, d->period, tiles, err, done, fs)
-                             : cudaLaunchKernelEx(&lc, dpd_main_kernel<32, kV, kThreads, false>, sub, tp, hist, d->period, tiles, err, done, fs));
+      const bool halo = fast && htail && base == 0;
+      cudaError_t le;
+      if (d->T == 10)
+        le = !fast ? cudaLaunchKernelEx(&lc, dpd_main_kernel<10, kV, kThreads, false, false>, sub, tp, hist, d->period, tiles, err, done, fs)
+             : halo ? cudaLaunchKernelEx(&lc, dpd_main_kernel<10, kV, kThreads, true, true>, sub, tp, hist, d->period, tiles, err, done, fs)
+                    : cudaLaunchKernelEx(&lc, dpd_main_kernel<10, kV, kThreads, true, false>, sub, tp, hist, d->period, tiles, err, done, fs);
+      else
+        le = !fast ? cudaLaunchKernelEx(&lc, dpd_main_kernel<32, kV, kThreads, false, false>, sub, tp, hist, d->period, tiles, err, done, fs)
+             : halo ? cudaLaunchKernelEx(&lc, dpd_main_kernel<32, kV, kThreads, true, true>, sub, tp, hist, d->period, tiles, err, done, fs)
+                    : cudaLaunchKernelEx(&lc, dpd_main_kernel<32, kV, kThreads, true, false>, sub, tp, hist, d->period, tiles, err, done, fs);
       DF_CHECK_CUDA(le);
       DF_TRY(after_launch("dpd_main_kernel"));
       // Later sub-launches continue from the state this one advanced (which
