@@ -197,7 +197,10 @@ int df_halo_copy(int dst_device, void* dst, int src_device, const void* src, siz
   if (dst_device == src_device) {
     DF_CHECK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, as_stream(stream)));
   } else {
-    DF_CHECK_CUDA(cudaMemcpyPeerAsync(dst, dst_device, src, src_device, bytes, as_stream(stream)));
+    // Unified addressing resolves both ends -- plain peer pointers and
+    // CUDA-IPC-mapped ones (df_ipc_open_handle) alike -- and the copy goes
+    // peer to peer over NVLink when peer access is enabled.
+    DF_CHECK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, as_stream(stream)));
   }
   return DF_OK;
 }
