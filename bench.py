@@ -137,8 +137,8 @@ HALO = os.environ.get("DF_BENCH_HALO", "ipc")
 class HaloPipe:
     """Double-buffered halo pulls on a side stream (peer copies
     overlapped with interior work).  pull(i, copies) issues step i's copies
-    [(dst_ptr_fn(slot), src_ptr, bytes)], and makes `stream` wait for them;
-    release(i) marks step i's slot consumed (after its consumer kernel)."""
+    [(dst_ptr, src_ptr, bytes)] into slot i % 2 and makes `stream` wait for
+    them; release(slot) marks the slot consumed (after its consumer kernel)."""
 
     def __init__(self, torch, stream, local, peer_device):
         self.torch, self.stream, self.local, self.peer = torch, stream, local, peer_device
@@ -383,12 +383,12 @@ def bench_dpd_ours(args, p, rank, world, local):
     # Block-range shard of a weak-scaled stream: rank r holds blocks
     # [r*blocks, (r+1)*blocks).  FIR-history halo: for each branch, the last
     # T-1 samples of its last active block in the previous rank's range
-    # (peer copies of the neighbour's mapped shard, or NCCL P2P; no
+    # (read in-kernel from the neighbour's mapped shard, or NCCL P2P; no
     # collective); rank 0 starts from zero history.
     from paper_1611_03226_b200 import shard
     H1 = max(T - 1, 1)
     tails = torch.zeros(10 * H1 * 2, dtype=torch.float32, device=dev)
-    halos = [torch.zeros_like(tails) for _ in range(2)]
+    halo = torch.zeros_like(tails)
     tail_src = []
     for b in range(1, 11):
         hb = shard.dpd_halo_block(sched, blocks, b)  # last active block of this rank (local index)
@@ -409,17 +409,14 @@ def bench_dpd_ours(args, p, rank, world, local):
 
     def step(ev0=None, ev1=None):
         sh = C.c_void_p(torch.cuda.current_stream().cuda_stream)  # the capture stream inside a graph
-        if world > 1 and tail_ptrs is None:
-            k, got = 0, rank > 0
-            if HALO != "ipc":
-                for b, hb in enumerate(tail_src):
-                    if hb is not None:
-                        a0 = 2 * ((hb + 1) * period - H1)
-                        tails[2 * H1 * b: 2 * H1 * (b + 1)].copy_(x[a0: a0 + 2 * H1])
-                got = shard.exchange_tail(tails, halos[0], rank, world)
-            if got:
+        if world > 1 and HALO != "ipc":  # NCCL P2P variant: exchange the tails, set the histories
+            for b, hb in enumerate(tail_src):
+                if hb is not None:
+                    a0 = 2 * ((hb + 1) * period - H1)
+                    tails[2 * H1 * b: 2 * H1 * (b + 1)].copy_(x[a0: a0 + 2 * H1])
+            if shard.exchange_tail(tails, halo, rank, world):
                 for b in range(10):
-                    _lib.call("df_dpd_set_history", actor.handle, C.c_void_p(halos[k].data_ptr() + 8 * H1 * b), H1,
+                    _lib.call("df_dpd_set_history", actor.handle, C.c_void_p(halo.data_ptr() + 8 * H1 * b), H1,
                               1 << b, sh)
         if ev0 is not None:
             ev0.record(stream)
