@@ -155,6 +155,36 @@ def test_fire_halo_shard_equals_full_run(gpu, T, period):
     assert_parity(out.download(np.float32), want[2 * period * b0:])
 
 
+@pytest.mark.parametrize("halo", [False, True])
+def test_batch_over_65535_blocks(gpu, halo):
+    """A firing of 70000 blocks is split into grid-sized sub-launches (grid.y
+    <= 65535); each continues from the FirState the previous one advanced
+    (and only the first takes the halo tails)."""
+    from paper_1611_03226_b200 import device, dpd
+    period, blocks, T = 16, 70000, 10
+    x = O.synth_samples(period * blocks, 4711)
+    taps = O.random_taps(4712, T)
+    rng = np.random.default_rng(4713)
+    sched = rng.integers(0, 1024, size=97).astype(np.uint16)
+    sched[60:] &= 0x1FF  # branch 10 gated off in a long stretch of every cycle
+    if not halo:
+        assert_parity(run_gpu(x, taps, sched, period), O.dpd(x, taps, sched, period))
+        return
+    b0 = 5
+    tails = _branch_tails(x, sched, period, b0, T)
+    bufs = [device.Buffer.from_array(t) if t is not None else None for t in tails]
+    a = dpd.DpdActor(period, taps)
+    nb = blocks - b0
+    ctrl = device.Buffer(4 * nb)
+    dpd.config_tokens(sched, b0, nb, ctrl)
+    inp = device.Buffer.from_array(x[2 * period * b0:])
+    out = device.Buffer(8 * period * nb)
+    a.fire_halo([bb.ptr.value if bb is not None else None for bb in bufs], ctrl, inp, out, nb)
+    a.check()
+    want = O.dpd(x, taps, sched, period)
+    assert_parity(out.download(np.float32), want[2 * period * b0:])
+
+
 def test_gating_invariance_acceptance9(gpu):
     # proj/tests/acceptance.cpp:398-450: branch 7 toggled; inactive periods
     # must be bit-identical when its taps change.
