@@ -46,6 +46,9 @@ WORKLOADS = {
     # name: (kind, params)
     "motion720": ("motion", dict(w=1280, h=720, frames=300, fmt=3, thr=32,
                                  label="Motion detection 1280x720 RGB, 300 synthetic frames per GPU")),
+    # The reference's own input format (8-bit gray, proj/include/dynflow/motion.hpp:11-16).
+    "motion720gray": ("motion", dict(w=1280, h=720, frames=300, fmt=1, thr=32,
+                                     label="Motion detection 1280x720 gray (reference format), 300 frames per GPU")),
     "motion4k": ("motion", dict(w=3840, h=2160, frames=40, fmt=3, thr=32,
                                 label="Motion detection 3840x2160 RGB, 40 frames per GPU (320 at 8 GPUs)")),
     "dpd1": ("dpd", dict(samples=1 << 20, period=65536, T=10, sched="first2",
@@ -305,7 +308,7 @@ def bench_motion_ours(args, p, rank, world, local):
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "u8",
-        "data": "synthetic (device splitmix64 bytes; RGB interleaved)",
+        "data": "synthetic (device splitmix64 bytes; " + ("RGB interleaved)" if fmt == 3 else "8-bit gray)"),
         "config": {"workload": p["label"], "width": W, "height": H, "frames_per_gpu": F,
                    "threshold": p["thr"], "input": "rgb" if fmt == 3 else "gray",
                    "chain": "gray->gauss5x5->|cur-prev|>thr->median5 (reference-pinned)",
@@ -505,21 +508,23 @@ def bench_dpd_ours(args, p, rank, world, local):
 
 # ------------------------------------------------------------------ CPU
 def cpu_motion(p, steps, warmup, threads=None, frames_per_net=None):
-    """Reference dynflow motion network (5 actor threads each) on gray(RGB),
-    several independent networks on disjoint frame ranges to use the host
-    cores; falls back to the single-thread oracle port."""
+    """Reference dynflow motion network (5 actor threads each) on gray(RGB)
+    (on the gray frames directly for a gray workload), several independent
+    networks on disjoint frame ranges to use the host cores; falls back to
+    the single-thread oracle port."""
     from oracle import oracle as O
     W, H = p["w"], p["h"]
+    rgb_in = p.get("fmt", 3) == 3
     ncpu = os.cpu_count() or 1
     if O.ref_available():
         R = O.ref()
         nets = threads or max(1, ncpu // 5)
         fpn = frames_per_net or 8
-        rgb = O.synth_bytes(fpn * W * H * 3, 5)
+        frames_in = O.synth_bytes(fpn * W * H * (3 if rgb_in else 1), 5)
         outs = [np.empty(fpn * W * H, np.uint8) for _ in range(nets)]
 
         def one(i):
-            gray = O.rgb_to_gray(rgb)
+            gray = O.rgb_to_gray(frames_in) if rgb_in else frames_in
             a, w_ = C.c_double(), C.c_double()
             R.ref_motion_network(gray.ctypes.data_as(C.c_void_p), fpn, W, H, 32, 1,
                                  outs[i].ctypes.data_as(C.c_void_p), C.byref(a), C.byref(w_))
@@ -538,13 +543,14 @@ def cpu_motion(p, steps, warmup, threads=None, frames_per_net=None):
         return {"value": round(nets * fpn / t, 2), "unit": "frames/s", "cores": min(ncpu, 5 * nets),
                 "kind": "reference",
                 "sample": f"{nets} concurrent dynflow motion networks (5 actor threads each) x {fpn} frames "
-                          f"{W}x{H}, gray(RGB) conversion included; median of {steps}"}
-    rgb = O.synth_bytes(4 * W * H * 3, 5)
+                          f"{W}x{H}" + (", gray(RGB) conversion included" if rgb_in else " gray")
+                          + f"; median of {steps}"}
+    frames_in = O.synth_bytes(4 * W * H * (3 if rgb_in else 1), 5)
     a = time.perf_counter()
-    O.motion_rgb(rgb, W, H)
+    (O.motion_rgb if rgb_in else O.motion_gray)(frames_in, W, H)
     t = time.perf_counter() - a
     return {"value": round(4 / t, 2), "unit": "frames/s", "cores": 1, "kind": "port",
-            "sample": f"oracle port, 4 frames {W}x{H} RGB, 1 thread"}
+            "sample": f"oracle port, 4 frames {W}x{H} {'RGB' if rgb_in else 'gray'}, 1 thread"}
 
 
 def cpu_dpd(p, steps, warmup):
