@@ -493,7 +493,8 @@ __device__ __forceinline__ void walk_frames(const MotionIO& io, const unsigned c
 #pragma unroll 10
     for (int r = 0; r < kBandRows + 2; ++r) {
       unsigned a0, a1;
-      load_bytes8<FAST>(prev_tok, y0 - 1 + r, x, g.W, g.H, a0, a1);
+      a0 = a1 = 0u;  // null token: black (proj/src/motion.cpp:131)
+      if (prev_tok) load_bytes8<FAST>(prev_tok, y0 - 1 + r, x, g.W, g.H, a0, a1);
       prev_s[r * 32 + lane] = make_uint2(a0, a1);
     }
   } else {
@@ -887,8 +888,8 @@ __device__ __forceinline__ void m3_walk(M3Stream<FMT, R>& st, const unsigned cha
   if (f_begin == 0 && !st.hfirst) {
     // Delay token: gauss of the previous firing's last frame -> TMEM.
     for (int r = 0; r < R + 2; ++r) {
-      unsigned a0, a1;
-      load_bytes8<true>(prev_tok, y0 - 1 + r, x, g.W, g.H, a0, a1);
+      unsigned a0 = 0u, a1 = 0u;  // null token: black (proj/src/motion.cpp:131)
+      if (prev_tok) load_bytes8<true>(prev_tok, y0 - 1 + r, x, g.W, g.H, a0, a1);
       tmem_st2(tmem + 2u * r, a0, a1);
     }
   } else {  // gauss(f_begin - 1): the previous frame, or the inline halo frame
@@ -1070,6 +1071,7 @@ struct df_motion {
   uint8_t thr = 32;
   unsigned char* tok[2] = {nullptr, nullptr};  // raw-mode delay token ping-pong
   int cur = 0;
+  bool black = false;  // the current token is the black initial token (not materialised)
   unsigned* scratch = nullptr;  // done counter
   int resident_ctas = 0;        // per SM, for the temporal chunking
   int m3_resident[3] = {0, 0, 0};  // motion_m3_kernel<R> CTAs per SM (0: M3 unavailable)
@@ -1334,10 +1336,11 @@ int df_motion_set_prev_frame(df_motion* m, const void* frame_dev, void* stream) 
   DF_REQUIRE(m, DF_EINVAL, "df_motion_set_prev_frame: null actor");
   DF_CHECK_CUDA(cudaSetDevice(m->device));
   cudaStream_t s = as_stream(stream);
-  if (!frame_dev) {
-    DF_CHECK_CUDA(cudaMemsetAsync(m->tok[m->cur], 0, (size_t)m->W * m->H, s));
+  if (!frame_dev) {  // black: the next firing loads zeros instead of a token
+    m->black = true;
     return DF_OK;
   }
+  m->black = false;
   dim3 grid((m->W + 127) / 128, m->H);
   if (m->fmt == DF_MOTION_RGB)
     gauss_frame_kernel<DF_MOTION_RGB><<<grid, 128, 0, s>>>((const unsigned char*)frame_dev, m->tok[m->cur], m->W, m->H);
@@ -1355,12 +1358,13 @@ int df_motion_fire(df_motion* m, const void* in_dev, uint8_t* out_dev, uint32_t 
   MotionIO io{};
   io.in = (const unsigned char*)in_dev;
   io.out = out_dev;
-  io.prev = m->tok[m->cur];
+  io.prev = m->black ? nullptr : m->tok[m->cur];
   io.next = m->tok[m->cur ^ 1];
   io.next_copy = nullptr;
   io.channel_mode = 0;
   DF_TRY(launch_motion(m, io, (int)frames, as_stream(stream)));
   m->cur ^= 1;
+  m->black = false;
   return DF_OK;
 }
 
@@ -1385,6 +1389,7 @@ int df_motion_fire_halo(df_motion* m, const void* halo_dev, const void* in_dev, 
   }
   DF_TRY(launch_motion(m, io, (int)frames, as_stream(stream)));
   m->cur ^= 1;
+  m->black = false;
   return DF_OK;
 }
 
