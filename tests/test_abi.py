@@ -60,3 +60,18 @@ def test_no_cpu_fallback_without_device():
     from paper_1611_03226_b200 import dpd
     with pytest.raises(P.CudaError):
         dpd.DpdActor(64, O.random_taps(1))
+
+
+def test_shard_entry_points_validate_arguments():
+    """df_*_fire_halo, df_ipc_* and df_halo_copy reject null handles/buffers
+    with DF_EINVAL before touching a device."""
+    from paper_1611_03226_b200 import _lib
+    lib = P.lib()
+    tails = (C.c_void_p * 10)()
+    buf = C.c_void_p(0x1000)
+    assert lib.df_motion_fire_halo(None, buf, buf, buf, 4, None) == _lib.DF_EINVAL
+    assert lib.df_dpd_fire_halo(None, tails, buf, buf, buf, 4, None) == _lib.DF_EINVAL
+    assert lib.df_ipc_get_handle(None, None) == _lib.DF_EINVAL
+    assert lib.df_ipc_open_handle(0, None, None) == _lib.DF_EINVAL
+    assert lib.df_ipc_handle_size() == 64  # cudaIpcMemHandle_t
+    assert b"null" in lib.df_last_error()
