@@ -622,6 +622,100 @@ def cpu_dpd(p, steps, warmup):
                       f"{n} samples each; median of {steps}"}
 
 
+# ------------------------------------------------------------------ networks
+def _timed_steps(step, steps, warmup, stream):
+    from paper_1611_03226_b200 import device
+    for _ in range(warmup):
+        step()
+    stream.synchronize()
+    e0, e1 = device.Event(), device.Event()
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    e1.synchronize()
+    return e0.elapsed_ms(e1) / steps
+
+
+def motion_network(p, steps, warmup):
+    """The motion actor inside its network on device channels: source ->
+    motion (input channel at rate F, rate-1 self-loop delay channel with the
+    black initial token, proj/src/motion.cpp:131) -> sink.  The source's
+    frames are resident in the input channel's storage (both Eq. 1 halves);
+    each step commits the source's write, fires the actor on the regions it
+    resolves on the device, and commits the sink's read (1-thread kernels)."""
+    from paper_1611_03226_b200 import _lib, device, motion
+    from paper_1611_03226_b200.channel import DeviceChannel
+    W, H, F, fmt = p["w"], p["h"], p["frames"], p["fmt"]
+    s = device.Stream()
+    cin = DeviceChannel(W * H * fmt, F)
+    cout = DeviceChannel(W * H, F)
+    delay = DeviceChannel(W * H, 1, has_delay=True, initial_token=np.zeros(W * H, np.uint8))
+    _lib.call("df_fill_random_u8", C.c_void_p(_lib.lib().df_channel_storage(cin.handle)), cin.capacity_bytes, 77,
+              s.handle)
+    a = motion.MotionActor(W, H, fmt, p["thr"])
+
+    def step():
+        wr = cin.write_start(F)
+        cin.write_end(wr, s)
+        a.fire_channels(cin, delay, cout, s)
+        rd = cout.read_start(F)
+        cout.read_end(rd, s)
+
+    ms = _timed_steps(step, steps, warmup, s)
+    for ch in (cin, cout, delay):
+        ch.check()
+    hbm, _ = peaks()
+    bytes_alg = (4.0 if fmt == 3 else 2.0) * W * H * F
+    return {"value": round(F / (ms / 1e3), 1), "unit": "frames/s", "ms_per_step": round(ms, 4),
+            "roofline_frac": round(bytes_alg / (ms / 1e3) / 1e9 / hbm, 4), "roofline_bound": "hbm",
+            "path": "source -> motion (device channels: Eq. 1 input/output rings at rate F, Fig. 2 delay "
+                    "self-loop; regions and commits on the device) -> sink; host-endpoint commits are 1-thread "
+                    "kernels; 3 launches per step"}
+
+
+def dpd_network(p, steps, warmup):
+    """The dynamic DPD actor inside its network on device channels: config
+    -> ctrl channel (4-byte control tokens, one per block) and source -> in
+    channel -> DPD (consumes K control tokens on the device) -> out channel
+    -> sink.  Tokens and samples are resident in both Eq. 1 halves."""
+    from paper_1611_03226_b200 import _lib, device, dpd
+    from paper_1611_03226_b200.channel import DeviceChannel
+    N, period, T = p["samples"], p["period"], p["T"]
+    K = N // period
+    sched = np.ascontiguousarray(dpd_schedule(p["sched"], K))
+    s = device.Stream()
+    cctl = DeviceChannel(4, K)
+    cin = DeviceChannel(8 * period, K)
+    cout = DeviceChannel(8 * period, K)
+    L = _lib.lib()
+    _lib.call("df_fill_random_pm1", C.c_void_p(L.df_channel_storage(cin.handle)), cin.capacity_bytes // 4, 99,
+              s.handle)
+    for half in range(cctl.capacity_tokens // K):
+        _lib.call("df_dpd_config_tokens", 0, sched.ctypes.data_as(C.c_void_p), sched.size, 0, K,
+                  C.c_void_p(L.df_channel_storage(cctl.handle) + 4 * K * half), s.handle)
+    taps = np.random.default_rng(808).uniform(-0.5, 0.5, size=(10, T, 2)).astype(np.float32)
+    a = dpd.DpdActor(period, taps)
+
+    def step():
+        for ch in (cctl, cin):
+            wr = ch.write_start(K)
+            ch.write_end(wr, s)
+        a.fire_channels(cctl, cin, cout, K, s)
+        rd = cout.read_start(K)
+        cout.read_end(rd, s)
+
+    ms = _timed_steps(step, steps, warmup, s)
+    a.check()
+    for ch in (cctl, cin, cout):
+        ch.check()
+    flops = dpd_flops_per_sample(sched, T) * N
+    return {"value": round(N / (ms / 1e3) / 1e6, 1), "unit": "Msamples/s", "ms_per_step": round(ms, 4),
+            "roofline_frac": round(flops / (ms / 1e3) / 1e12 / 37.2, 4), "roofline_bound": "fp32",
+            "path": "config -> ctrl channel, source -> in channel -> dpd (control tokens consumed on the device) "
+                    "-> out channel -> sink; host-endpoint commits are 1-thread kernels"}
+
+
 def bench_reference(args, kind, p, rank, world):
     if rank != 0:
         return None
@@ -671,6 +765,9 @@ def main():
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
             res["cpu_baseline"] = (cpu_motion(p, 3, 1) if kind == "motion" else cpu_dpd(p, 3, 1))
+        if world == 1 and not args.no_secondary and args.workload in ("motion720", "motion4k", "dpd3"):
+            # the same actor inside its on-device network (device channels)
+            res["network"] = (motion_network if kind == "motion" else dpd_network)(p, args.steps, args.warmup)
         if world == 1 and kind == "motion" and not args.no_secondary:
             # BASELINE's metric also names DPD Msamples/s: the DPD configs
             # (configs[0], [2], [4] per GPU) measured the same way, compactly.
@@ -686,6 +783,8 @@ def main():
                              "roofline": {k: r["roofline"][k] for k in ("bound", "achieved", "peak", "unit", "frac",
                                                                         "hbm_frac", "traffic")},
                              "cpu_baseline": cb}
+                if name == "dpd3":
+                    sec[name]["network"] = dpd_network(WORKLOADS[name][1], 5, 3)
             res["secondary"] = sec
         print(json.dumps(res), flush=True)
     if world > 1:
