@@ -1,0 +1,42 @@
+"""CPU: bench.py's workload table and algorithmic-work formulas match the
+BASELINE configs and SURVEY 8(d) (no GPU needed)."""
+import json
+import os
+
+import pytest
+
+import bench
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_workloads_cover_baseline_configs():
+    cfg = json.load(open(os.path.join(ROOT, "BASELINE.json")))["configs"]
+    assert len(cfg) == 5
+    w = bench.WORKLOADS
+    assert w["dpd1"][1]["samples"] == 1 << 20 and w["dpd1"][1]["T"] == 10 and w["dpd1"][1]["sched"] == "first2"
+    assert w["motion720"][1]["w"] == 1280 and w["motion720"][1]["h"] == 720 and w["motion720"][1]["frames"] == 300
+    assert w["motion720"][1]["fmt"] == 3  # RGB, as configs[1] states
+    assert w["dpd3"][1]["period"] == 4096 and w["dpd3"][1]["sched"] == "ramp"
+    assert w["motion4k"][1]["w"] == 3840 and w["motion4k"][1]["frames"] * 8 == 320
+    assert w["dpd5"][1]["T"] == 32 and w["dpd5"][1]["samples"] * 8 == 1 << 30
+
+
+@pytest.mark.parametrize("name,want", [("dpd1", 173), ("dpd3", 470), ("dpd5", 2613)])
+def test_dpd_flops_per_sample_matches_survey(name, want):
+    p = bench.WORKLOADS[name][1]
+    sched = bench.dpd_schedule(p["sched"], p["samples"] // p["period"])
+    assert abs(bench.dpd_flops_per_sample(sched, p["T"]) - want) < 1.0
+
+
+def test_ramp_schedule_is_1_to_10_branches():
+    s = bench.dpd_schedule("ramp", 20)
+    assert [bin(int(m)).count("1") for m in s] == list(range(1, 11))
+    assert all(int(m) == (1 << bin(int(m)).count("1")) - 1 for m in s)  # first_n(k)
+
+
+def test_default_run_is_n1_motion720():
+    src = open(os.path.join(ROOT, "bench.py")).read()
+    assert 'ap.add_argument("--gpus", type=int, default=1)' in src
+    assert 'ap.add_argument("--workload", default="motion720"' in src
+    assert "args.warmup = max(args.warmup, 3)" in src
