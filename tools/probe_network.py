@@ -45,7 +45,12 @@ def commits_only():
     cin.read_end(rd, s)
 
 
-for name, fn in (("bare firing, stream launches", bare), ("network step", network)):
+def channel_firing_only():  # timing only: without the endpoint commits the channel state is violated
+    a.fire_channels(cin, delay, cout, s)
+
+
+for name, fn in (("bare firing, stream launches", bare), ("network step", network),
+                 ("channel-bound firing alone (state violated; timing only)", channel_firing_only)):
     print(f"{name}: {bench._timed_steps(fn, 20, 5, s) * 1e3:.1f} us")
 cin2 = DeviceChannel(16, 4)
 def two_commits():
