@@ -367,7 +367,10 @@ __global__ void __launch_bounds__(THREADS, dpd_min_blocks<T>()) dpd_main_kernel(
       }
     }
     // History before the block start: the branch's frozen FIR state as
-    // resolved by the prep kernel (u[-(j+1)] at window index H1-1-j).
+    // resolved by the prep kernel (u[-(j+1)] at window index H1-1-j).  It
+    // overwrites the zero-padded poly slots 0..H1-1, stored above by other
+    // lanes of warp 0: order the two stores (block-start tiles only).
+    if (tile == 0) __syncwarp();
     if (has_hist) u[hslot] = hb[(b - 1) * H1];
     if (C::WL)
       __syncwarp();
