@@ -271,7 +271,10 @@ int df_motion_median5(const uint8_t* in_dev, uint8_t* out_dev, unsigned w, unsig
 int df_motion_rgb_to_gray(const uint8_t* rgb_dev, uint8_t* gray_dev, size_t pixels,
                           void* stream);
 
-/* ---- multi-GPU halos (NVLink peer copies; no collectives) --------------- */
+/* ---- multi-GPU halos (NVLink peer copies; no collectives) ---------------
+ * No reference counterpart: dynflow is one CPU process.  These serve the
+ * frame-range / block-range sharding of the two actors (one process per
+ * GPU; df_motion_fire_halo / df_dpd_fire_halo take the halos). */
 int df_peer_enable(int device_a, int device_b);
 int df_halo_copy(int dst_device, void* dst, int src_device, const void* src, size_t bytes,
                  void* stream);
