@@ -440,12 +440,17 @@ def bench_dpd_ours(args, p, rank, world, local):
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     graph = None
     launches0 = device.kernel_launches()
-    if world == 1:
-        graph = torch.cuda.CUDAGraph()  # K steps, one graph (see bench_motion_ours)
+    if world == 1 or HALO == "ipc":
+        # K steps, one graph (see bench_motion_ours).  At N > 1 the IPC
+        # transport needs no per-step communication (the firing reads its
+        # halo over NVLink), so the steps are pure launches and capture too.
+        graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
             for _ in range(args.steps):
                 step()
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
     launches = device.kernel_launches() - launches0
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
