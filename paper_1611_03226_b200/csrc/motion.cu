@@ -173,15 +173,22 @@ __device__ __forceinline__ unsigned thres4(unsigned cur, unsigned prev, const Mo
   return lop_maj(t, d, g.thr_sel);
 }
 
-// Majority of 5 (bitwise): centre c, up u, down d, left l, right r.
+__device__ __forceinline__ unsigned lop_xor3(unsigned a, unsigned b, unsigned c) {
+  unsigned d;
+  asm("lop3.b32 %0, %1, %2, %3, 0x96;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+// Majority of 5 (bitwise): centre c, up u, down d, left l, right r, in 5
+// LOP3: a full adder of (c, u, d) gives the count 2*s1 + s0, and the count
+// plus l + r reaches 3 iff s1 ? (s0 | l | r) : (s0 & l & r).  (The select
+// over any/majority/all of (c, u, d) by (l, r) takes 6; A/B in
+// profiles/r01_ab_motion_variants.txt.)
 __device__ __forceinline__ unsigned maj5(unsigned c, unsigned u, unsigned d, unsigned l,
                                          unsigned r) {
-  const unsigned any3 = lop_or3(c, u, d);
-  const unsigned m3 = lop_maj(c, u, d);
-  const unsigned all3 = lop_and3(c, u, d);
-  const unsigned X = lop_sel(r, any3, m3);
-  const unsigned Y = lop_sel(r, m3, all3);
-  return lop_sel(l, X, Y);
+  const unsigned s0 = lop_xor3(c, u, d);
+  const unsigned s1 = lop_maj(c, u, d);
+  return lop_sel(s1, lop_or3(s0, l, r), lop_and3(s0, l, r));
 }
 
 // --- row I/O -----------------------------------------------------------
