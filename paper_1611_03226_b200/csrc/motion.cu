@@ -601,6 +601,9 @@ constexpr size_t kSmemBytes = sizeof(uint2) * kWarpsPerCta * (kBandRows + 2) * 3
 // gauss/thres/median work) instead of right before their use: A/B
 // (profiles/r01_ab_motion_variants.txt) 4K R=59 -1.8 %, 720p R=54 +1.3 %
 // (ptxas allocates R=54 at the 128-register cap), so per band height.
+#ifndef DF_M3_MINB
+#define DF_M3_MINB 4  // __launch_bounds__ min blocks (register cap 65536 / (128 * MINB))
+#endif
 #ifndef DF_M3_EARLY_MIN_R
 #define DF_M3_EARLY_MIN_R 59
 #endif
@@ -910,7 +913,7 @@ __device__ __forceinline__ void m3_walk(M3Stream<FMT, R>& st, const unsigned cha
 }
 
 template <int FMT, int R>
-__global__ void __launch_bounds__(32 * kM3Warps, 4) motion_m3_kernel(const __grid_constant__ CUtensorMap map,
+__global__ void __launch_bounds__(32 * kM3Warps, DF_M3_MINB) motion_m3_kernel(const __grid_constant__ CUtensorMap map,
                                                                    const __grid_constant__ CUtensorMap hmap,
                                                                    MotionIO io, MotionGeom g,
                                                                    unsigned* done_counter) {
