@@ -185,6 +185,25 @@ def test_batch_over_65535_blocks(gpu, halo):
     assert_parity(out.download(np.float32), want[2 * period * b0:])
 
 
+def test_run_host_schedule_change_between_runs(gpu):
+    """df_dpd_run_host reuses the control tokens of an identical schedule and
+    regenerates them when the schedule (same length) or the block count
+    changes."""
+    from paper_1611_03226_b200 import dpd
+    period, T = 256, 10
+    taps = O.random_taps(55, T)
+    a = dpd.DpdActor(period, taps)
+    sa = np.array([0x3FF, 0x001, 0x0F0], np.uint16)
+    sb = np.array([0x002, 0x300, 0x155], np.uint16)
+    for sched, blocks in ((sa, 12), (sb, 12), (sa, 12), (sa, 7), (sb, 7)):
+        x = O.synth_samples(period * blocks, int(sched[0]) + blocks)
+        a.reset()
+        out = np.empty_like(x)
+        a.run_host(x, out, sched)
+        a.check()
+        assert_parity(out, O.dpd(x, taps, sched, period))
+
+
 def test_gating_invariance_acceptance9(gpu):
     # proj/tests/acceptance.cpp:398-450: branch 7 toggled; inactive periods
     # must be bit-identical when its taps change.
