@@ -17,7 +17,7 @@ rgb.array[:] = O.synth_bytes(F * W * H * 3, 1)
 out = device.PinnedArray(F * W * H, np.uint8)
 a = motion.MotionActor(W, H, motion.RGB, 32)
 a.run_host(rgb.array, out.array)
-t = time.perf_counter(); a.run_host(rgb.array, out.array); t1 = time.perf_counter() - t
+t = time.perf_counter(); a.run_host(rgb.array, out.array); t_motion_pinned = t1 = time.perf_counter() - t
 a2 = motion.MotionActor(W, H, motion.RGB, 32)  # fresh delay token (black), like a new network run
 a2.run_host(rgb.array, out.array)
 ref = out.array.copy()
@@ -56,3 +56,16 @@ for rate in (10, 60):
     got, sink_ms, _ = host_api.motion_run(pg_in, W, H, fmt=3, rate=rate)
     t2 = time.perf_counter() - t
     print(f"pageable buffers, dfh_motion_run rate {rate}: wall {F / t2:.0f} fps, sink-active {F / (sink_ms / 1e3):.0f} fps")
+
+# df_*_run_host with pageable caller buffers (staged through pinned slots
+# with parallel host copies) vs pinned
+pg_out = np.empty(F * W * H, np.uint8)
+a3 = motion.MotionActor(W, H, motion.RGB, 32)
+a3.run_host(pg_in, pg_out)
+t = time.perf_counter(); a3.run_host(pg_in, pg_out); t3 = time.perf_counter() - t
+print(f"run_host, pageable buffers: {F / t3:.0f} fps (pinned: {F / t_motion_pinned:.0f})")
+pgx = np.array(x.array)
+pgy = np.empty_like(pgx)
+d.run_host(pgx, pgy, sched)
+t = time.perf_counter(); d.run_host(pgx, pgy, sched); t4 = time.perf_counter() - t
+print(f"dpd run_host, pageable buffers: {N / t4 / 1e6:.0f} Msps")
