@@ -184,6 +184,12 @@ __host__ __device__ constexpr int pad_index(int w) { return w + (w >> 3); }  // 
 template <int T>
 constexpr int dpd_min_blocks() { return T <= 16 ? 5 : 0; }
 
+// 1: every CTA of a plain fast-path firing takes part in the end-of-grid
+// done count (the A/B baseline); 0: only the block-start tiles do.
+#ifndef DF_DPD_TAIL_ALL
+#define DF_DPD_TAIL_ALL 0
+#endif
+
 // Warp-local windows for T <= DF_DPD_WARP_MAX_T: DPD-3 -1 % (1.165 vs 1.176
 // ms); T=32 would need 164 registers (3 CTAs/SM) and runs DPD-5 8 % slower
 // (profiles/r01_ab_dpd_variants.txt).
@@ -446,15 +452,21 @@ __global__ void __launch_bounds__(THREADS, dpd_min_blocks<T>()) dpd_main_kernel(
   // waited on it, and every batch has one, so no other CTA needs to: they
   // retire and free their slots while prep may still be running.
 
-  if (io.channel_mode || fast) {
-    // Last CTA: advances the FirState (fast path; every other CTA has read
-    // the old one) and commits the firing batch: K control tokens, K block
-    // tokens consumed, K block tokens produced (ports always at full rate).
+  // Only block-start tiles read the carried FirState and last1, so on a
+  // plain fast-path firing only they are counted (gridDim.y of them) and
+  // every other CTA retires here without the fence and the atomic; a
+  // channel firing counts every CTA, since its commit publishes all outputs.
+  const bool counted = io.channel_mode || (fast && (DF_DPD_TAIL_ALL || tile == 0));
+  if (counted) {
+    // Last counted CTA: advances the FirState (fast path; every block-start
+    // tile has read the old one) and commits the firing batch: K control
+    // tokens, K block tokens consumed, K block tokens produced (ports always
+    // at full rate).
     __shared__ bool last;
     __syncthreads();
     if (tid == 0) {
       __threadfence();
-      const unsigned total = gridDim.x * gridDim.y;
+      const unsigned total = io.channel_mode || DF_DPD_TAIL_ALL ? gridDim.x * gridDim.y : gridDim.y;
       last = atomicAdd(done_counter, 1u) == total - 1;
     }
     __syncthreads();
