@@ -36,8 +36,9 @@
 // Fast path (period >= T-1, every BASELINE config): the history of block p
 // is the tail of ONE block -- the branch's last earlier active block q -- so
 // the main kernel resolves it itself: each block-start tile scans the
-// control tokens back from p with warp ballots, and the grid's last CTA
-// advances the FirState from the per-branch last active block (atomicMax).
+// control tokens back from p with warp ballots, and the last block-start
+// tile to finish advances the FirState from the per-branch last active
+// block (atomicMax).
 // One launch per batch, no history table.
 #include <algorithm>
 #include <cstring>
