@@ -9,11 +9,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
 
-from oracle import oracle as O
 from paper_1611_03226_b200 import device, dpd
 
 N, period = 1 << 20, 65536
-actor = dpd.DpdActor(period, O.random_taps(808))
+actor = dpd.DpdActor(period, np.random.default_rng(808).uniform(-0.5, 0.5, (10, 10, 2)).astype(np.float32))
 hin = device.PinnedArray(2 * N, np.float32)
 hout = device.PinnedArray(2 * N, np.float32)
 hin.array[:] = np.random.default_rng(0).uniform(-1, 1, 2 * N).astype(np.float32)

@@ -8,12 +8,11 @@ import time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 
-from oracle import oracle as O
 from paper_1611_03226_b200 import device, dpd, host_api, motion
 
 W, H, F = 1280, 720, 300
 rgb = device.PinnedArray(F * W * H * 3, np.uint8)
-rgb.array[:] = O.synth_bytes(F * W * H * 3, 1)
+rgb.array[:] = np.random.default_rng(1).integers(0, 256, F * W * H * 3, dtype=np.uint8)
 out = device.PinnedArray(F * W * H, np.uint8)
 a = motion.MotionActor(W, H, motion.RGB, 32)
 a.run_host(rgb.array, out.array)
@@ -32,8 +31,8 @@ for rate in (10, 30, 60, 150, 300):
 
 N, period = 1 << 20, 65536
 x = device.PinnedArray(2 * N, np.float32)
-x.array[:] = O.synth_samples(N, 810)
-taps = O.random_taps(808)
+x.array[:] = np.random.default_rng(810).uniform(-1, 1, 2 * N).astype(np.float32)
+taps = np.random.default_rng(808).uniform(-0.5, 0.5, (10, 10, 2)).astype(np.float32)
 d = dpd.DpdActor(period, taps)
 y = device.PinnedArray(2 * N, np.float32)
 sched = np.array([3], np.uint16)

@@ -10,7 +10,6 @@ import time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 
-from oracle import oracle as O
 from paper_1611_03226_b200 import _lib, device, dpd
 
 
@@ -26,7 +25,7 @@ def t(fn, reps=20):
 
 for name, N, period, T, sched in (("dpd1", 1 << 20, 65536, 10, [3]), ("dpd3", 1 << 26, 4096, 10, [(1 << (1 + i % 10)) - 1 for i in range(10)]),
                                   ("dpd5", 1 << 27, 65536, 32, [0x3FF])):
-    taps = O.random_taps(808) if T == 10 else np.random.default_rng(1).uniform(-0.5, 0.5, (10, T, 2)).astype(np.float32)
+    taps = np.random.default_rng(808).uniform(-0.5, 0.5, (10, 10, 2)).astype(np.float32) if T == 10 else np.random.default_rng(1).uniform(-0.5, 0.5, (10, T, 2)).astype(np.float32)
     actor = dpd.DpdActor(period, taps)
     hin = device.PinnedArray(2 * N, np.float32)
     hout = device.PinnedArray(2 * N, np.float32)
