@@ -185,6 +185,10 @@ __host__ __device__ constexpr int pad_index(int w) { return w + (w >> 3); }  // 
 template <int T>
 constexpr int dpd_min_blocks() { return T <= 16 ? 5 : 0; }
 
+#ifndef DF_DPD_BLOCK_MAJOR
+#define DF_DPD_BLOCK_MAJOR 1
+#endif
+
 // 1: every CTA of a plain fast-path firing takes part in the end-of-grid
 // done count (the A/B baseline); 0: only the block-start tiles do.
 #ifndef DF_DPD_TAIL_ALL
@@ -248,7 +252,7 @@ __device__ __forceinline__ float2 carried_history(const FastState& fs, int bi, i
 template <int T, int V, int THREADS, bool FAST, bool HALO>
 __global__ void __launch_bounds__(THREADS, dpd_min_blocks<T>()) dpd_main_kernel(DpdIO io, const float2* __restrict__ taps_g,
                                                             const float2* __restrict__ hist,
-                                                            unsigned period, unsigned tiles_per_block,
+                                                            unsigned period, unsigned block_major,
                                                             unsigned* err, unsigned* done_counter,
                                                             FastState fs) {
   using C = MainCfg<T, V, THREADS>;
@@ -259,8 +263,11 @@ __global__ void __launch_bounds__(THREADS, dpd_min_blocks<T>()) dpd_main_kernel(
   __shared__ float2 hist_s[FAST ? kBranches * HS : 1];  // fast path: this block's history per branch
   __shared__ int q_s[kBranches];
 
-  const unsigned long long p = blockIdx.y;
-  const unsigned tile = blockIdx.x;
+  // Block-major grids (fast path) index blocks on x, so the block-start
+  // tiles -- the only CTAs with history and FirState work -- are
+  // dispatched first and the grid never ends on one of them.
+  const unsigned long long p = block_major ? blockIdx.x : blockIdx.y;
+  const unsigned tile = block_major ? blockIdx.y : blockIdx.x;
   const uint32_t* ctrl = io_ctrl(io);
   const float2* __restrict__ x = io_in(io);
   float2* __restrict__ y = io_out(io);
@@ -454,7 +461,7 @@ __global__ void __launch_bounds__(THREADS, dpd_min_blocks<T>()) dpd_main_kernel(
   // retire and free their slots while prep may still be running.
 
   // Only block-start tiles read the carried FirState and last1, so on a
-  // plain fast-path firing only they are counted (gridDim.y of them) and
+  // plain fast-path firing only they are counted (one per block) and
   // every other CTA retires here without the fence and the atomic; a
   // channel firing counts every CTA, since its commit publishes all outputs.
   const bool counted = io.channel_mode || (fast && (DF_DPD_TAIL_ALL || tile == 0));
@@ -467,7 +474,9 @@ __global__ void __launch_bounds__(THREADS, dpd_min_blocks<T>()) dpd_main_kernel(
     __syncthreads();
     if (tid == 0) {
       __threadfence();
-      const unsigned total = io.channel_mode || DF_DPD_TAIL_ALL ? gridDim.x * gridDim.y : gridDim.y;
+      const unsigned total = io.channel_mode || DF_DPD_TAIL_ALL ? gridDim.x * gridDim.y
+                             : block_major                    ? gridDim.x
+                                                              : gridDim.y;
       last = atomicAdd(done_counter, 1u) == total - 1;
     }
     __syncthreads();
@@ -594,6 +603,7 @@ __global__ void dpd_config_kernel(const uint16_t* __restrict__ sched, unsigned l
 #endif
 constexpr int kV = DF_DPD_V;              // consecutive outputs per thread
 constexpr int kThreads = DF_DPD_THREADS;  // threads per CTA (tile = kV * kThreads samples)
+constexpr unsigned long long kBlockMajorMaxCtas = 4096;  // ~5.5 waves at 5 CTAs/SM
 
 }  // namespace
 }  // namespace df
@@ -681,7 +691,13 @@ int launch_dpd(df_dpd* d, const DpdIO& io, unsigned long long K, cudaStream_t s,
       }
       const float2* hist = d->hist + base * kBranches * (d->T - 1);
       cudaLaunchConfig_t lc{};
-      lc.gridDim = dim3(tiles, (unsigned)k);
+      // Block-major only for short grids (a few waves), where the grid's
+      // end is the block-start tiles' FirState hand-off: DPD-1 (1024 CTAs)
+      // 16.1 -> 14.1 us; DPD-3 (65536 CTAs) is 0.5 % slower block-major
+      // (profiles/r01_ab_dpd_variants.txt).
+      const unsigned bm =
+          fast && DF_DPD_BLOCK_MAJOR && tiles <= 65535u && k * tiles <= kBlockMajorMaxCtas ? 1u : 0u;
+      lc.gridDim = bm ? dim3((unsigned)k, tiles) : dim3(tiles, (unsigned)k);
       lc.blockDim = dim3(kThreads);
       lc.dynamicSmemBytes = 0;
       lc.stream = s;
@@ -694,13 +710,13 @@ int launch_dpd(df_dpd* d, const DpdIO& io, unsigned long long K, cudaStream_t s,
       const bool halo = fast && htail && base == 0;
       cudaError_t le;
       if (d->T == 10)
-        le = !fast ? cudaLaunchKernelEx(&lc, dpd_main_kernel<10, kV, kThreads, false, false>, sub, tp, hist, d->period, tiles, err, done, fs)
-             : halo ? cudaLaunchKernelEx(&lc, dpd_main_kernel<10, kV, kThreads, true, true>, sub, tp, hist, d->period, tiles, err, done, fs)
-                    : cudaLaunchKernelEx(&lc, dpd_main_kernel<10, kV, kThreads, true, false>, sub, tp, hist, d->period, tiles, err, done, fs);
+        le = !fast ? cudaLaunchKernelEx(&lc, dpd_main_kernel<10, kV, kThreads, false, false>, sub, tp, hist, d->period, bm, err, done, fs)
+             : halo ? cudaLaunchKernelEx(&lc, dpd_main_kernel<10, kV, kThreads, true, true>, sub, tp, hist, d->period, bm, err, done, fs)
+                    : cudaLaunchKernelEx(&lc, dpd_main_kernel<10, kV, kThreads, true, false>, sub, tp, hist, d->period, bm, err, done, fs);
       else
-        le = !fast ? cudaLaunchKernelEx(&lc, dpd_main_kernel<32, kV, kThreads, false, false>, sub, tp, hist, d->period, tiles, err, done, fs)
-             : halo ? cudaLaunchKernelEx(&lc, dpd_main_kernel<32, kV, kThreads, true, true>, sub, tp, hist, d->period, tiles, err, done, fs)
-                    : cudaLaunchKernelEx(&lc, dpd_main_kernel<32, kV, kThreads, true, false>, sub, tp, hist, d->period, tiles, err, done, fs);
+        le = !fast ? cudaLaunchKernelEx(&lc, dpd_main_kernel<32, kV, kThreads, false, false>, sub, tp, hist, d->period, bm, err, done, fs)
+             : halo ? cudaLaunchKernelEx(&lc, dpd_main_kernel<32, kV, kThreads, true, true>, sub, tp, hist, d->period, bm, err, done, fs)
+                    : cudaLaunchKernelEx(&lc, dpd_main_kernel<32, kV, kThreads, true, false>, sub, tp, hist, d->period, bm, err, done, fs);
       DF_CHECK_CUDA(le);
       DF_TRY(after_launch("dpd_main_kernel"));
       // Later sub-launches continue from the state this one advanced (which
