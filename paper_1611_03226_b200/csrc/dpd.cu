@@ -185,6 +185,9 @@ __host__ __device__ constexpr int pad_index(int w) { return w + (w >> 3); }  // 
 template <int T>
 constexpr int dpd_min_blocks() { return T <= 16 ? 5 : 0; }
 
+#ifndef DF_DPD_PREFETCH
+#define DF_DPD_PREFETCH 1
+#endif
 #ifndef DF_DPD_BLOCK_MAJOR
 #define DF_DPD_BLOCK_MAJOR 1
 #endif
@@ -252,7 +255,7 @@ __device__ __forceinline__ float2 carried_history(const FastState& fs, int bi, i
 template <int T, int V, int THREADS, bool FAST, bool HALO>
 __global__ void __launch_bounds__(THREADS, dpd_min_blocks<T>()) dpd_main_kernel(DpdIO io, const float2* __restrict__ taps_g,
                                                             const float2* __restrict__ hist,
-                                                            unsigned period, unsigned block_major,
+                                                            unsigned period, unsigned block_major, unsigned ahead,
                                                             unsigned* err, unsigned* done_counter,
                                                             FastState fs) {
   using C = MainCfg<T, V, THREADS>;
@@ -273,6 +276,21 @@ __global__ void __launch_bounds__(THREADS, dpd_min_blocks<T>()) dpd_main_kernel(
   float2* __restrict__ y = io_out(io);
 
   const int tid = threadIdx.x;
+  // L2 prefetch of the input tile of the CTA dispatched `ahead` (= the
+  // resident CTA slots) after this one: it starts about when this CTA
+  // retires, and finds its input in L2 instead of waiting on HBM.
+  if (DF_DPD_PREFETCH && ahead && tid == 0) {
+    const unsigned long long L = blockIdx.x + (unsigned long long)blockIdx.y * gridDim.x + ahead;
+    if (L < (unsigned long long)gridDim.x * gridDim.y) {
+      const unsigned gx = (unsigned)(L % gridDim.x), gy = (unsigned)(L / gridDim.x);
+      const unsigned long long pp = block_major ? gx : gy;
+      const unsigned ts = (block_major ? gy : gx) * C::S;
+      const unsigned bytes = (min((unsigned)C::S, period - ts) * 8u) & ~15u;
+      const float2* src = x + pp * period + ts;
+      if (bytes && ((reinterpret_cast<uintptr_t>(src) & 15u) == 0))
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+    }
+  }
   // Window-local thread index and the window's first output in the tile.
   const int lt = C::WL ? (tid & 31) : tid;
   const int wb = C::WL ? (tid >> 5) * C::OW : 0;
@@ -616,6 +634,7 @@ struct df_dpd {
   uint32_t T = 10;
   float2* taps = nullptr;      // device, 10*T
   float2* state = nullptr;     // device, 10*(kMaxTaps-1): FirState per branch
+  unsigned resident_ctas = 0;  // main-kernel CTAs resident on the device (prefetch distance)
   unsigned* scratch = nullptr; // [0] error word, [1] done counter, [4..13] fast-path last1
   float2* hist = nullptr;      // device history table, capacity hist_blocks
   int* act = nullptr;          // device active lists, 10*hist_blocks
@@ -697,6 +716,10 @@ int launch_dpd(df_dpd* d, const DpdIO& io, unsigned long long K, cudaStream_t s,
       // (profiles/r01_ab_dpd_variants.txt).
       const unsigned bm =
           fast && DF_DPD_BLOCK_MAJOR && tiles <= 65535u && k * tiles <= kBlockMajorMaxCtas ? 1u : 0u;
+      // Next-wave L2 prefetch, also for short grids only: DPD-1 -2.5 %;
+      // DPD-3 +0.8 % and DPD-5 +1.6 % (already latency-hidden; A/B in
+      // profiles/r01_ab_dpd_variants.txt).
+      const unsigned ahead = DF_DPD_PREFETCH && k * tiles <= kBlockMajorMaxCtas ? d->resident_ctas : 0u;
       lc.gridDim = bm ? dim3((unsigned)k, tiles) : dim3(tiles, (unsigned)k);
       lc.blockDim = dim3(kThreads);
       lc.dynamicSmemBytes = 0;
@@ -710,13 +733,13 @@ int launch_dpd(df_dpd* d, const DpdIO& io, unsigned long long K, cudaStream_t s,
       const bool halo = fast && htail && base == 0;
       cudaError_t le;
       if (d->T == 10)
-        le = !fast ? cudaLaunchKernelEx(&lc, dpd_main_kernel<10, kV, kThreads, false, false>, sub, tp, hist, d->period, bm, err, done, fs)
-             : halo ? cudaLaunchKernelEx(&lc, dpd_main_kernel<10, kV, kThreads, true, true>, sub, tp, hist, d->period, bm, err, done, fs)
-                    : cudaLaunchKernelEx(&lc, dpd_main_kernel<10, kV, kThreads, true, false>, sub, tp, hist, d->period, bm, err, done, fs);
+        le = !fast ? cudaLaunchKernelEx(&lc, dpd_main_kernel<10, kV, kThreads, false, false>, sub, tp, hist, d->period, bm, ahead, err, done, fs)
+             : halo ? cudaLaunchKernelEx(&lc, dpd_main_kernel<10, kV, kThreads, true, true>, sub, tp, hist, d->period, bm, ahead, err, done, fs)
+                    : cudaLaunchKernelEx(&lc, dpd_main_kernel<10, kV, kThreads, true, false>, sub, tp, hist, d->period, bm, ahead, err, done, fs);
       else
-        le = !fast ? cudaLaunchKernelEx(&lc, dpd_main_kernel<32, kV, kThreads, false, false>, sub, tp, hist, d->period, bm, err, done, fs)
-             : halo ? cudaLaunchKernelEx(&lc, dpd_main_kernel<32, kV, kThreads, true, true>, sub, tp, hist, d->period, bm, err, done, fs)
-                    : cudaLaunchKernelEx(&lc, dpd_main_kernel<32, kV, kThreads, true, false>, sub, tp, hist, d->period, bm, err, done, fs);
+        le = !fast ? cudaLaunchKernelEx(&lc, dpd_main_kernel<32, kV, kThreads, false, false>, sub, tp, hist, d->period, bm, ahead, err, done, fs)
+             : halo ? cudaLaunchKernelEx(&lc, dpd_main_kernel<32, kV, kThreads, true, true>, sub, tp, hist, d->period, bm, ahead, err, done, fs)
+                    : cudaLaunchKernelEx(&lc, dpd_main_kernel<32, kV, kThreads, true, false>, sub, tp, hist, d->period, bm, ahead, err, done, fs);
       DF_CHECK_CUDA(le);
       DF_TRY(after_launch("dpd_main_kernel"));
       // Later sub-launches continue from the state this one advanced (which
@@ -762,6 +785,15 @@ int df_dpd_create(int device, uint32_t period, uint32_t T, const float* taps_hos
   if (e == cudaSuccess) e = cudaMemcpy(d->taps, taps_host, sizeof(float2) * kBranches * T, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemset(d->state, 0, sizeof(float2) * kBranches * (kMaxTaps - 1));
   if (e == cudaSuccess) e = cudaMemset(d->scratch, 0, 64);
+  if (e == cudaSuccess && (T == 10 || T == 32)) {  // resident main-kernel CTAs: the L2 prefetch distance
+    int per_sm = 0, sms = 0;
+    e = T == 10 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dpd_main_kernel<10, kV, kThreads, true, false>,
+                                                                kThreads, 0)
+                : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dpd_main_kernel<32, kV, kThreads, false, false>,
+                                                                kThreads, 0);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    d->resident_ctas = (unsigned)(per_sm * sms);
+  }
   if (e != cudaSuccess) {
     int rc = cuda_status(e, "df_dpd_create");
     cudaFree(d->taps);
