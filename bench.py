@@ -426,7 +426,7 @@ def bench_dpd_ours(args, p, rank, world, local):
                     _lib.call("df_dpd_set_history", actor.handle, C.c_void_p(halo.data_ptr() + 8 * H1 * b), H1,
                               1 << b, sh)
         if ev0 is not None:
-            ev0.record(stream)
+            ev0.record(torch.cuda.current_stream())
         if tail_ptrs is not None:
             _lib.call("df_dpd_fire_halo", actor.handle, tail_ptrs, C.c_void_p(ctrl.data_ptr()),
                       C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), blocks, sh)
@@ -434,7 +434,7 @@ def bench_dpd_ours(args, p, rank, world, local):
             _lib.call("df_dpd_fire", actor.handle, C.c_void_p(ctrl.data_ptr()), C.c_void_p(x.data_ptr()),
                       C.c_void_p(y.data_ptr()), blocks, sh)
         if ev1 is not None:
-            ev1.record(stream)
+            ev1.record(torch.cuda.current_stream())
 
     for _ in range(args.warmup):
         step()
@@ -450,19 +450,26 @@ def bench_dpd_ours(args, p, rank, world, local):
     # event times.
     l2_flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev) if 16 * N < L2_FLUSH_BYTES else None
     launches0 = device.kernel_launches()
-    if l2_flush is None and (world == 1 or HALO == "ipc"):
+    # Per-step events; captured into the graph as event-record nodes
+    # (external) when the steps are flushed and timed one by one.
+    kev = [(torch.cuda.Event(enable_timing=True, external=True), torch.cuda.Event(enable_timing=True, external=True))
+           for _ in range(args.steps)]
+    if world == 1 or HALO == "ipc":
         # K steps, one graph (see bench_motion_ours).  At N > 1 the IPC
         # transport needs no per-step communication (the firing reads its
         # halo over NVLink), so the steps are pure launches and capture too.
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
-            for _ in range(args.steps):
-                step()
+            for i in range(args.steps):
+                if l2_flush is not None:
+                    l2_flush.fill_(i & 0xFF)
+                    step(*kev[i])
+                else:
+                    step()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
     launches = device.kernel_launches() - launches0
-    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
         t0.record(stream)
         if graph is not None:
@@ -477,7 +484,8 @@ def bench_dpd_ours(args, p, rank, world, local):
     if graph is None:
         launches = device.kernel_launches() - launches0
     ms = max_over_ranks(t0.elapsed_time(t1) / args.steps, world)
-    kms = ms if graph is not None else max_over_ranks(statistics.mean(a.elapsed_time(b) for a, b in kev), world)
+    kms = ms if graph is not None and l2_flush is None else max_over_ranks(
+        statistics.mean(a.elapsed_time(b) for a, b in kev), world)
     if l2_flush is not None:
         ms = kms  # the flushes between steps are not part of the step
     actor.check()
