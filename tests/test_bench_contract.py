@@ -40,3 +40,18 @@ def test_default_run_is_n1_motion720():
     assert 'ap.add_argument("--gpus", type=int, default=1)' in src
     assert 'ap.add_argument("--workload", default="motion720"' in src
     assert "args.warmup = max(args.warmup, 3)" in src
+
+
+def test_l2_rule_every_workload_flushes_or_exceeds_l2():
+    """Timing rule: between timed steps either flush L2 or use data larger
+    than L2 (126 MB).  DPD workloads below L2_FLUSH_BYTES are flushed; every
+    other workload's input alone exceeds L2."""
+    l2 = 126e6
+    assert bench.L2_FLUSH_BYTES > l2
+    for name, (kind, p) in bench.WORKLOADS.items():
+        if kind == "dpd":
+            flushed = 16 * p["samples"] < bench.L2_FLUSH_BYTES
+            assert flushed or 8 * p["samples"] > l2, name
+            assert flushed == (name == "dpd1"), name
+        else:
+            assert p["w"] * p["h"] * p["fmt"] * p["frames"] > l2, name
