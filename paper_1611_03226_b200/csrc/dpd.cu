@@ -298,14 +298,17 @@ __global__ void __launch_bounds__(THREADS, dpd_min_blocks<T>()) dpd_main_kernel(
   const unsigned t0 = tile * C::S;
   const int n = (int)min((unsigned)C::S, period - t0);  // valid outputs in this tile
   const size_t blk = (size_t)p * period;
-  uint32_t mask = ctrl[p];
-  if (mask >> kBranches) {
-    if (tid == 0) atomicCAS(err, 0u, (unsigned)DF_ECONTROL);
-    mask &= (1u << kBranches) - 1;
+  // Every global load of the prologue (taps, control token, the window's
+  // inputs) is issued before any of them is consumed, so a CTA waits one
+  // memory latency, not three in a row.
+  constexpr int NTR = (kBranches * T + THREADS - 1) / THREADS;  // taps per thread
+  float2 tr[NTR];
+#pragma unroll
+  for (int k = 0; k < NTR; ++k) {
+    const int i = tid + k * THREADS;
+    if (i < kBranches * T) tr[k] = __ldg(&taps_g[i]);
   }
-
-  for (int i = tid; i < kBranches * T; i += THREADS) taps_s[i] = taps_g[i];
-
+  uint32_t mask = ctrl[p];
   // Window position w in [0, W): sample index t0 + wb - (T-1) + w of the
   // block.  Each thread owns positions w = lt + m*L; keeps x, mag, scale.
   float xr[C::M], xi[C::M], mg[C::M], sc[C::M];
@@ -317,7 +320,19 @@ __global__ void __launch_bounds__(THREADS, dpd_min_blocks<T>()) dpd_main_kernel(
     if (w < C::W && wb + w < n + H1 && s >= 0) v = __ldg(&x[blk + s]);
     xr[m] = v.x;
     xi[m] = v.y;
-    mg[m] = __fsqrt_rn(__fadd_rn(__fmul_rn(v.x, v.x), __fmul_rn(v.y, v.y)));
+  }
+#pragma unroll
+  for (int k = 0; k < NTR; ++k) {
+    const int i = tid + k * THREADS;
+    if (i < kBranches * T) taps_s[i] = tr[k];
+  }
+  if (mask >> kBranches) {
+    if (tid == 0) atomicCAS(err, 0u, (unsigned)DF_ECONTROL);
+    mask &= (1u << kBranches) - 1;
+  }
+#pragma unroll
+  for (int m = 0; m < C::M; ++m) {
+    mg[m] = __fsqrt_rn(__fadd_rn(__fmul_rn(xr[m], xr[m]), __fmul_rn(xi[m], xi[m])));
     sc[m] = 1.0f;
   }
 
