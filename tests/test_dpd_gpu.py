@@ -340,3 +340,20 @@ def test_block_shard_with_history_halo(gpu):
         a.fire(ctrl, xb, out, rest, in_offset=8 * period * s_block)
         got = out.download(np.float32)
         assert_parity(got, full[2 * period * s_block:])
+
+
+@pytest.mark.parametrize("T", [10, 32])
+def test_grid_orders_agree(gpu, T):
+    """Short firings (<= 4096 CTAs) run block-major with a next-wave L2
+    prefetch, long ones tile-major: the same stream fired as one 8192-CTA
+    batch and in 64-block chunks must be bit-identical, and match the oracle
+    (a ramp plus gated-off stretches exercises the FirState hand-off)."""
+    period, blocks = 4096, 2048  # 4 tiles per block: 8192 CTAs in one batch
+    x = O.synth_samples(period * blocks, 2100 + T)
+    taps = O.random_taps(2200 + T, T)
+    sched = np.array([(1 << (1 + i % 10)) - 1 for i in range(10)] + [1, 0x200, 0x3FF, 2], np.uint16)
+    whole = run_gpu(x, taps, sched, period, chunk_blocks=blocks)
+    chunked = run_gpu(x, taps, sched, period, chunk_blocks=64)
+    assert np.array_equal(bits(whole), bits(chunked))
+    n = 96 * period
+    assert_parity(whole[:2 * n], O.dpd(x[:2 * n], taps, sched, period))
