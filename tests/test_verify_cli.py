@@ -95,3 +95,20 @@ def test_dpd_verify_passes_cli(gpu):
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert r.stdout == "app=dpd\nseed=43\nverify=PASS\n"
+
+
+def test_dpd_fail_reports_first_divergent_sample(monkeypatch):
+    """DPD FAIL path: a device result off by 1e-3 relative at sample 4100 (no GPU needed)."""
+
+    def fake_dpd_run(x, taps, schedule, period, device):
+        y = O.dpd(x, taps, schedule, period)
+        y[2 * 4100] = y[2 * 4100] * (1 + 1e-3) + 1e-3
+        return y, 0.0, 0
+
+    monkeypatch.setattr(host_api, "dpd_run", fake_dpd_run)
+    out = io.StringIO()
+    rc = V.verify(args("--app", "dpd", "--samples", "8192", "--period", "1024", "--seed", "5"), out)
+    assert rc == V.EXIT_VERIFY_FAILED
+    lines = out.getvalue().splitlines()
+    assert lines[0] == "verify dpd (seed 5): FAIL"
+    assert lines[1].startswith("first divergence: sample 4100: got (")
