@@ -30,7 +30,14 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 HBM_FALLBACK_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
-FP32_PEAK_TOPS = 148 * 128 * 1.965e9 / 1e12  # non-fused FP32 issue peak at max clock
+# Non-fused FP32 peak, MEASURED on the box (not in MEASURED_PEAKS.json):
+# tools/ubench_ops.cu issued FMUL at 1106.0 and FADD at 1114.8 G warp-
+# instructions/s on 148 SMs (profiles/r01_box_probe_and_pipe_ubench.log),
+# i.e. 35.4 / 35.7 Top/s; the mean is the denominator.  The theoretical
+# 148 x 128 x 1.965 GHz = 37.2 Top/s is reported beside it.
+FP32_PEAK_TOPS = 32 * (1106.0 + 1114.8) / 2 / 1e3
+FP32_PEAK_SOURCE = "measured (tools/ubench_ops FMUL/FADD, profiles/r01_box_probe_and_pipe_ubench.log)"
+FP32_THEORETICAL_TOPS = 148 * 128 * 1.965e9 / 1e12
 
 
 def peaks():
@@ -526,8 +533,10 @@ def bench_dpd_ours(args, p, rank, world, local):
                 "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * N,
                 "path": "df_dpd_run_host (C ABI, pinned host buffers)"},
         "gpu_launches": int(launches),
-        "roofline": {"bound": "fp32", "achieved": round(achieved_tops, 2), "peak": round(FP32_PEAK_TOPS, 1),
+        "roofline": {"bound": "fp32", "achieved": round(achieved_tops, 2), "peak": round(FP32_PEAK_TOPS, 2),
                      "unit": "Top/s (non-fused FP32)", "frac": round(achieved_tops / FP32_PEAK_TOPS, 4),
+                     "peak_source": FP32_PEAK_SOURCE,
+                     "frac_of_theoretical": round(achieved_tops / FP32_THEORETICAL_TOPS, 4),
                      "traffic": traffic_from_profiles("dpd_main_kernel", args.workload),
                      "kernel_ms": round(kms, 4), "flops_per_sample": fps,
                      "hbm_frac": round(16 * N / (kms / 1e3) / 1e9 / hbm, 4)},
@@ -740,7 +749,7 @@ def dpd_network(p, steps, warmup):
         ch.check()
     flops = dpd_flops_per_sample(sched, T) * N
     return {"value": round(N / (ms / 1e3) / 1e6, 1), "unit": "Msamples/s", "ms_per_step": round(ms, 4),
-            "roofline_frac": round(flops / (ms / 1e3) / 1e12 / 37.2, 4), "roofline_bound": "fp32",
+            "roofline_frac": round(flops / (ms / 1e3) / 1e12 / FP32_PEAK_TOPS, 4), "roofline_bound": "fp32",
             "path": "config -> ctrl channel, source -> in channel -> dpd (control tokens consumed on the device) "
                     "-> out channel -> sink; host-endpoint commits are 1-thread kernels"}
 

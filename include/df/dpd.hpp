@@ -31,9 +31,11 @@ struct ConfigToken {
   static ConfigToken first_n(unsigned k) { return {static_cast<std::uint16_t>((1u << k) - 1)}; }
 };
 
-// check_config (dpd.cpp:49-58) with the single-branch extension:
-// k in [min_active, 10], no branch beyond 10.
-void check_config(ConfigToken token, unsigned min_active = 1);
+// check_config (dpd.cpp:49-58): k in [min_active, 10], no branch beyond
+// 10.  The reference's bound is k >= 2 (the default); min_active = 1 is the
+// single-branch extension BASELINE's ramp schedule needs (its oracle
+// accepts any mask), enabled only through Params::allow_single_branch.
+void check_config(ConfigToken token, unsigned min_active = 2);
 
 struct Params {
   std::uint32_t period = 65536;       // samples per token (one block)
@@ -42,6 +44,7 @@ struct Params {
   std::vector<std::complex<float>> taps;  // 10 * taps_per_branch, branch-major
   std::vector<ConfigToken> schedule;      // one entry per block, cycling
   std::uint32_t batch = 1;                // logical firings per launch
+  bool allow_single_branch = false;       // k = 1 masks (extension; reference: k >= 2)
   std::span<const std::complex<float>> input;  // host, interleaved re/im
   std::span<std::complex<float>> output;
 };

@@ -184,8 +184,27 @@ NetworkGraph build_network(std::vector<ActorSpec> actors, std::vector<ChannelSpe
 // Rule checks, ordered by channel id, actor id, then structure
 // (model.cpp:104-238): rates/sizes >= 1, initial tokens only with a delay,
 // control channels rate 1 without delay, one control port per dynamic
-// actor, no undelayed cycles.  A delayed self-loop is legal.
+// actor, no undelayed cycles.  A delayed self-loop is legal at rate 1; a
+// cycle whose delay channels all have rate > 1 is reported too (it cannot
+// fire: the reference would block in read_start forever).
 std::vector<Violation> validate(const NetworkGraph& net);
+
+// Does the channel order firing i of its producer before firing i of its
+// consumer?  Every channel except a rate-1 delay channel: its one initial
+// token shifts the stream by a whole firing (consumer firing i reads what
+// producer firing i-1 wrote); at rate r > 1 the consumer's firing i still
+// needs r-1 tokens of producer firing i.
+bool orders_same_firing(const ChannelSpec& spec);
+
+// A topological order of the actors over the channels selected by
+// orders_same_firing (declaration order among independent actors), or
+// nullopt when they form a cycle.  The static schedule issues firing i of
+// every actor in this order.
+std::optional<std::vector<std::size_t>> firing_order(const NetworkGraph& net);
+
+// One "a -> b -> a" path per cyclic component of the graph of channels
+// selected by `edge` (validate()'s cycle findings).
+std::vector<std::string> cycles(const NetworkGraph& net, const std::function<bool(const ChannelSpec&)>& edge);
 
 // Eq. 1 (channel.cpp:9-16).
 std::size_t capacity_tokens(const ChannelSpec& spec);

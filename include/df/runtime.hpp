@@ -9,8 +9,13 @@
 // firing i of every actor in topological order -- and encodes the channel
 // protocol as stream/event dependencies:
 //   * data:      consumer firing i waits for the producer's firing i;
-//   * capacity:  producer firing i waits for the consumer's firing i - P
-//                (P = 2 buffer phases, 3 with a delay token: Eq. 1);
+//   * capacity:  producer firing i waits for the consumer's firing i - 2,
+//                for both layouts.  Regular channels alternate two halves, so
+//                write i reuses the half read i-2 released.  A delay channel
+//                (3r+1 slots) write i overlaps the region read i-2 held as
+//                well: reads start one slot lower than writes, and the phase-2
+//                copy into slot 0 overwrites the first slot of read phase 0.
+//                Lag 3 would race; lag 2 is the correct bound for both.
 // while token COUNTS (0 or r per port for dynamic actors) and region
 // addresses live on the device (df_channel).  The host synchronizes once,
 // at the end.  Device-side contract violations (token underflow/overflow,

@@ -209,7 +209,10 @@ int df_dpd_config_tokens(int device, const uint16_t* schedule_host, size_t sched
 /* End to end from HOST buffers (drop-in for oracle_dpd / cmd_dpd's run):
  * samples % period == 0; H2D, config tokens, firings and D2H are pipelined
  * in chunks of `chunk_blocks` blocks on `stream` plus internal copy streams.
- * Continues from the actor's current FIR history (call df_dpd_reset for a
+ * Continues from the actor's current FIR history and from its schedule
+ * position: block i of this call is governed by schedule[(n + i) % len],
+ * n = blocks fired by earlier run_host calls since create / df_dpd_reset, so
+ * one stream split over several calls equals one call (df_dpd_reset starts a
  * fresh run).  Synchronizes before returning. */
 int df_dpd_run_host(df_dpd* dpd, const float* in_host, float* out_host, uint64_t samples,
                     const uint16_t* schedule_host, size_t schedule_len, uint64_t chunk_blocks,

@@ -22,12 +22,14 @@ extern "C" {
 const char* dfh_last_error(void);
 
 /* taps: 10 * taps_per_branch complex (re, im) floats, branch-major;
- * schedule: one 10-bit mask per block (bit b-1 = branch b), cycling.
+ * schedule: one 10-bit mask per block (bit b-1 = branch b), cycling, each
+ * with 2..10 active branches as the reference's check_config demands
+ * (src/dpd.cpp:49-58), or 1..10 with allow_single_branch (extension).
  * samples % (period * batch) == 0.  sink_active_ms: device time of the
  * sink actor from its first to its last firing (like active_seconds). */
 int dfh_dpd_run(int device, const float* in_host, float* out_host, uint64_t samples, uint32_t period,
                 uint32_t taps_per_branch, const float* taps, const uint16_t* schedule, size_t schedule_len,
-                uint32_t batch, double* sink_active_ms, uint64_t* dpd_firings);
+                uint32_t batch, int allow_single_branch, double* sink_active_ms, uint64_t* dpd_firings);
 
 /* input_format: 1 gray, 3 RGB; frames % token_rate == 0. */
 int dfh_motion_run(int device, const uint8_t* in_host, uint8_t* out_host, uint64_t frames, unsigned width,
@@ -55,7 +57,15 @@ int dfh_memory(int app, unsigned width, unsigned height, uint32_t token_rate, ui
 /* Host-side rule checks (no device): builds the named reference network
  * shape and returns the number of validate() violations (0 = runnable);
  * -1 with dfh_last_error() on a BuildError / invalid_argument. */
-int dfh_validate_demo(int which);  /* which: 0..4, see host_abi.cpp */
+int dfh_validate_demo(int which);  /* which: 0..6, see host_abi.cpp */
+
+/* Ordering check of the static schedule (device needed): source -> sink
+ * over ONE delay channel of 8-byte tokens at token_rate, initial token all
+ * 0xFF bytes, the sink optionally declared first.  Source firing i writes
+ * the values i*r+1 .. i*r+r; out_host receives the sink's firings*r tokens:
+ * the initial token, then 1, 2, ... (a delay channel of rate r > 1 orders
+ * the producer's firing i before the consumer's firing i). */
+int dfh_delay_chain_run(int device, uint32_t token_rate, int sink_first, uint64_t firings, uint64_t* out_host);
 
 #ifdef __cplusplus
 }

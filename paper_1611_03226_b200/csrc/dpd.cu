@@ -660,7 +660,12 @@ struct df_dpd {
   uint16_t* sched_dev = nullptr;
   size_t sched_cap = 0;
   std::vector<uint16_t> sched_host;    // schedule the tokens in ctrl_buf were made from
-  unsigned long long ctrl_blocks = 0;  // ... and their count
+  unsigned long long ctrl_blocks = 0;  // ... their count
+  unsigned long long ctrl_first = 0;   // ... and the schedule position of the first
+  // Blocks df_dpd_run_host has fired since create / reset: the config
+  // actor's firing index (dpd.cpp:208 schedule[firing % len]) continues
+  // from here, so a stream split over several calls sees one schedule.
+  unsigned long long run_blocks = 0;
   df::Staging staging;  // df_dpd_run_host pipeline
 };
 
@@ -850,6 +855,7 @@ int df_dpd_reset(df_dpd* d, void* stream) {
   DF_CHECK_CUDA(cudaSetDevice(d->device));
   DF_CHECK_CUDA(cudaMemsetAsync(d->state, 0, sizeof(float2) * kBranches * (kMaxTaps - 1), as_stream(stream)));
   DF_CHECK_CUDA(cudaMemsetAsync(d->scratch, 0, 64, as_stream(stream)));
+  d->run_blocks = 0;
   return DF_OK;
 }
 
@@ -1001,20 +1007,24 @@ int df_dpd_run_host(df_dpd* d, const float* in_host, float* out_host, uint64_t s
     d->sched_cap = schedule_len;
   }
   uint32_t* ctrl = static_cast<uint32_t*>(d->ctrl_buf);
-  // Config actor: one control token per block, on device.  A stream of runs
-  // with the same schedule and length reuses the tokens already in HBM.
-  const bool same = d->ctrl_blocks == blocks &&
+  // Config actor: one control token per block, on device, continuing the
+  // schedule from the blocks earlier calls fired.  A stream of runs with the
+  // same schedule, length and schedule position reuses the tokens in HBM.
+  const unsigned long long first = d->run_blocks % schedule_len;
+  const bool same = d->ctrl_blocks == blocks && d->ctrl_first == first &&
                     d->sched_host.size() == schedule_len &&
                     std::memcmp(d->sched_host.data(), schedule_host, schedule_len * sizeof(uint16_t)) == 0;
   if (!same) {
     DF_CHECK_CUDA(cudaMemcpyAsync(d->sched_dev, schedule_host, schedule_len * sizeof(uint16_t),
                                   cudaMemcpyHostToDevice, cs));
     dpd_config_kernel<<<(unsigned)std::min<uint64_t>((blocks + 255) / 256, 1184), 256, 0, cs>>>(
-        d->sched_dev, (unsigned)schedule_len, 0, blocks, ctrl);
+        d->sched_dev, (unsigned)schedule_len, first, blocks, ctrl);
     DF_TRY(after_launch("dpd_config_kernel"));
     d->sched_host.assign(schedule_host, schedule_host + schedule_len);
     d->ctrl_blocks = blocks;
+    d->ctrl_first = first;
   }
+  d->run_blocks += blocks;
   const uint64_t nchunks = (blocks + chunk_blocks - 1) / chunk_blocks;
   auto nb = [&](uint64_t c) { return std::min(chunk_blocks, blocks - c * chunk_blocks); };
   return d->staging.pipeline(

@@ -12,7 +12,7 @@ namespace df::dpd {
 
 void check_config(ConfigToken token, unsigned min_active) {
   // dpd.cpp:49-58 (the reference network requires k >= 2; k = 1 is the
-  // north-star extension, its oracle accepts any mask)
+  // north-star extension, its oracle accepts any mask; see dpd.hpp)
   if (token.active_mask >> kBranchCount) throw std::invalid_argument("config token names a branch beyond 10");
   const unsigned k = token.active_count();
   if (k < min_active || k > kBranchCount)
@@ -29,7 +29,7 @@ NetworkGraph build_network(const Params& p) {
   if (p.samples == 0 || p.samples % launch != 0)
     throw std::invalid_argument("dpd: sample count must be a nonzero multiple of period * batch");
   if (p.schedule.empty()) throw std::invalid_argument("dpd: schedule must not be empty");
-  for (ConfigToken t : p.schedule) check_config(t, 1);
+  for (ConfigToken t : p.schedule) check_config(t, p.allow_single_branch ? 1 : 2);
   if (p.taps_per_branch < 1 || p.taps_per_branch > 32)
     throw std::invalid_argument("dpd: taps per branch outside [1,32]");
   if (p.taps.size() != std::size_t(kBranchCount) * p.taps_per_branch)

@@ -1,11 +1,13 @@
 // host_abi.cpp -- extern "C" entry points of libdf_host.so (df_host.h).
 #include <complex>
 #include <cstring>
+#include <memory>
 #include <string>
 
 #include "df/dpd.hpp"
 #include "df/motion.hpp"
 #include "df/runtime.hpp"
+#include "df_cuda.h"
 #include "df_host.h"
 
 namespace {
@@ -47,7 +49,7 @@ const char* dfh_last_error(void) { return g_err.c_str(); }
 
 int dfh_dpd_run(int device, const float* in_host, float* out_host, uint64_t samples, uint32_t period,
                 uint32_t T, const float* taps, const uint16_t* schedule, size_t schedule_len, uint32_t batch,
-                double* sink_active_ms, uint64_t* dpd_firings) {
+                int allow_single_branch, double* sink_active_ms, uint64_t* dpd_firings) {
   return guarded([&] {
     df::dpd::Params p;
     p.period = period;
@@ -57,6 +59,7 @@ int dfh_dpd_run(int device, const float* in_host, float* out_host, uint64_t samp
     for (std::size_t i = 0; i < p.taps.size(); ++i) p.taps[i] = {taps[2 * i], taps[2 * i + 1]};
     for (size_t i = 0; i < schedule_len; ++i) p.schedule.push_back({schedule[i]});
     p.batch = batch;
+    p.allow_single_branch = allow_single_branch != 0;
     p.input = {reinterpret_cast<const std::complex<float>*>(in_host), samples};
     p.output = {reinterpret_cast<std::complex<float>*>(out_host), samples};
     df::NetworkGraph net = df::dpd::build_network(p);
@@ -229,6 +232,44 @@ int dfh_memory(int app, unsigned width, unsigned height, uint32_t rate, uint32_t
   return rc == 0 ? n : -1;
 }
 
+int dfh_delay_chain_run(int device, uint32_t rate, int sink_first, uint64_t firings, uint64_t* out_host) {
+  return guarded([&] {
+    using namespace df;
+    // source --(delay channel, rate r, initial token 0xFFFF...)--> sink.
+    // Source firing i writes tokens with values i*r+1 .. i*r+r; the sink
+    // reads r tokens per firing: the initial token, then the stream.
+    auto values = std::make_shared<std::vector<std::uint64_t>>(firings * rate);
+    for (std::size_t i = 0; i < values->size(); ++i) (*values)[i] = i + 1;
+    std::vector<std::byte> init(8, std::byte{0xFF});
+    std::vector<ChannelSpec> chans = {{"d", 8, rate, true, init}};
+    ActorBehavior src, snk;
+    src.fire = [values, rate](FiringContext& ctx) {
+      df_region r;
+      check(df_channel_write_start(ctx.output(0), rate, &r));
+      check(df_memcpy_h2d(r.dptr, values->data() + ctx.firing_index() * rate, 8ull * rate, ctx.stream()));
+      check(df_channel_write_end(ctx.output(0), &r, ctx.stream()));
+    };
+    snk.fire = [out_host, rate](FiringContext& ctx) {
+      df_region r;
+      check(df_channel_read_start(ctx.input(0), rate, &r));
+      check(df_memcpy_d2h(out_host + ctx.firing_index() * rate, r.dptr, 8ull * rate, ctx.stream()));
+      check(df_channel_read_end(ctx.input(0), &r, ctx.stream()));
+    };
+    ActorSpec a_src{"source", ActorKind::static_rate, {{PortDirection::output, PortKind::regular, "d"}}, src};
+    ActorSpec a_snk{"sink", ActorKind::static_rate, {{PortDirection::input, PortKind::regular, "d"}}, snk};
+    std::vector<ActorSpec> actors;
+    if (sink_first) {
+      actors = {a_snk, a_src};
+    } else {
+      actors = {a_src, a_snk};
+    }
+    ExecutionConfig cfg;
+    cfg.device = device;
+    cfg.source_firing_limit = firings;
+    run(build_network(actors, chans), cfg);
+  });
+}
+
 int dfh_validate_demo(int which) {
   int n = -1;
   int rc = guarded([&] {
@@ -244,6 +285,7 @@ int dfh_validate_demo(int which) {
       p.batch = 2;
       p.taps = taps;
       p.schedule = {dpd::ConfigToken::first_n(1), dpd::ConfigToken::first_n(10)};
+      p.allow_single_branch = true;
       p.input = io;
       p.output = io;
       n = (int)validate(dpd::build_network(p)).size();
@@ -297,6 +339,29 @@ int dfh_validate_demo(int which) {
       both.fire = noop;
       both.host_fire = [](HostFiringContext&) {};
       actors.push_back({"both", ActorKind::static_rate, {{PortDirection::input, PortKind::regular, "e"}}, both});
+      n = (int)validate(build_network(actors, chans)).size();
+      return;
+    }
+    if (which == 5 || which == 6) {  // cycles whose delay channels have rate 2: unrunnable
+      ActorBehavior b;
+      b.fire = noop;
+      if (which == 5) {  // a -> b undelayed, b -> a delayed at rate 2
+        chans = {{"ab", 4, 2, false, {}}, {"ba", 4, 2, true, {}}};
+        actors.push_back({"a", ActorKind::static_rate,
+                          {{PortDirection::output, PortKind::regular, "ab"},
+                           {PortDirection::input, PortKind::regular, "ba"}},
+                          b});
+        actors.push_back({"b", ActorKind::static_rate,
+                          {{PortDirection::input, PortKind::regular, "ab"},
+                           {PortDirection::output, PortKind::regular, "ba"}},
+                          b});
+      } else {  // delayed self-loop at rate 2
+        chans = {{"loop", 8, 2, true, {}}};
+        actors.push_back({"m", ActorKind::static_rate,
+                          {{PortDirection::input, PortKind::regular, "loop"},
+                           {PortDirection::output, PortKind::regular, "loop"}},
+                          b});
+      }
       n = (int)validate(build_network(actors, chans)).size();
       return;
     }

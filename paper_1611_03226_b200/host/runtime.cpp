@@ -128,31 +128,6 @@ void fire_host_actor(ActorRun& r, std::uint64_t firing, HostFaults& faults, std:
   for (std::size_t k = 0; k < nin; ++k) check(df_channel_read_end(r.ctx.input(k), &rin[k], r.stream));
 }
 
-// Topological order over undelayed channels (validate() rejected cycles).
-std::vector<std::size_t> topo_order(const NetworkGraph& net) {
-  const std::size_t n = net.actors().size();
-  std::vector<int> indeg(n, 0);
-  std::vector<std::vector<std::size_t>> next(n);
-  for (std::size_t c = 0; c < net.channels().size(); ++c) {
-    if (net.channels()[c].has_delay) continue;
-    const auto& ep = net.endpoints()[c];
-    if (ep.producer_actor == ep.consumer_actor) continue;
-    next[ep.producer_actor].push_back(ep.consumer_actor);
-    ++indeg[ep.consumer_actor];
-  }
-  std::vector<std::size_t> order, ready;
-  for (std::size_t a = 0; a < n; ++a)
-    if (indeg[a] == 0) ready.push_back(a);
-  while (!ready.empty()) {
-    std::size_t a = ready.front();
-    ready.erase(ready.begin());
-    order.push_back(a);
-    for (std::size_t b : next[a])
-      if (--indeg[b] == 0) ready.push_back(b);
-  }
-  return order;
-}
-
 }  // namespace
 
 RunStats run(const NetworkGraph& net, const ExecutionConfig& cfg) {
@@ -240,7 +215,8 @@ RunStats run(const NetworkGraph& net, const ExecutionConfig& cfg) {
     throw;
   }
 
-  const std::vector<std::size_t> order = topo_order(net);
+  // validate() rejected every cycle of same-firing channels.
+  const std::vector<std::size_t> order = firing_order(net).value();
   const std::uint64_t limit = cfg.source_firing_limit.value_or(0);
   std::string fault_actor;
   HostFaults host_faults;

@@ -26,13 +26,14 @@ def lib():
         L = C.CDLL(HOST_LIB_PATH)
         L.dfh_last_error.restype = C.c_char_p
         L.dfh_dpd_run.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_void_p,
-                                  C.c_void_p, C.c_size_t, C.c_uint32, C.POINTER(C.c_double),
+                                  C.c_void_p, C.c_size_t, C.c_uint32, C.c_int, C.POINTER(C.c_double),
                                   C.POINTER(C.c_uint64)]
         L.dfh_motion_run.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint, C.c_uint, C.c_int,
                                      C.c_uint8, C.c_uint32, C.POINTER(C.c_double), C.POINTER(C.c_uint64)]
         L.dfh_motion_run_mixed.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint, C.c_uint,
                                            C.c_uint8, C.c_uint32, C.c_void_p, C.c_int64, C.POINTER(C.c_double)]
         L.dfh_validate_demo.argtypes = [C.c_int]
+        L.dfh_delay_chain_run.argtypes = [C.c_int, C.c_uint32, C.c_int, C.c_uint64, C.c_void_p]
         L.dfh_memory.argtypes = [C.c_int, C.c_uint, C.c_uint, C.c_uint32, C.c_uint32, C.c_int,
                                  C.POINTER(C.c_uint64)]
         _h = L
@@ -45,8 +46,10 @@ def _check(rc):
 
 
 def dpd_run(inp: np.ndarray, taps: np.ndarray, schedule, period: int, batch: int = 1, device: int = 0,
-            out: np.ndarray | None = None):
-    """run(dpd::build_network(params)) on the GPU; returns (output, sink_active_ms, dpd_firings)."""
+            out: np.ndarray | None = None, allow_single_branch: bool = False):
+    """run(dpd::build_network(params)) on the GPU; returns (output, sink_active_ms, dpd_firings).
+    Masks must have 2..10 active branches (the reference's check_config), or
+    1..10 with allow_single_branch (extension)."""
     inp = np.ascontiguousarray(inp, np.float32).reshape(-1)
     taps = np.ascontiguousarray(taps, np.float32)
     T = taps.shape[1]
@@ -55,7 +58,7 @@ def dpd_run(inp: np.ndarray, taps: np.ndarray, schedule, period: int, batch: int
     ms, fir = C.c_double(0), C.c_uint64(0)
     _check(lib().dfh_dpd_run(device, inp.ctypes.data_as(C.c_void_p), out.ctypes.data_as(C.c_void_p), inp.size // 2,
                              period, T, taps.ctypes.data_as(C.c_void_p), sched.ctypes.data_as(C.c_void_p),
-                             sched.size, batch, C.byref(ms), C.byref(fir)))
+                             sched.size, batch, int(allow_single_branch), C.byref(ms), C.byref(fir)))
     return out, ms.value, fir.value
 
 
@@ -99,3 +102,11 @@ def memory(app: str, shape: str, width: int = 320, height: int = 240, rate: int 
 
 def validate_demo(which: int) -> int:
     return int(lib().dfh_validate_demo(which))
+
+
+def delay_chain_run(rate: int, sink_first: bool, firings: int, device: int = 0) -> np.ndarray:
+    """source -> sink over one delay channel (dfh_delay_chain_run); returns
+    the sink's tokens as uint64 (initial token 2^64-1, then 1, 2, ...)."""
+    out = np.zeros(firings * rate, np.uint64)
+    _check(lib().dfh_delay_chain_run(device, rate, int(sink_first), firings, out.ctypes.data_as(C.c_void_p)))
+    return out

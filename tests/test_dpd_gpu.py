@@ -204,6 +204,31 @@ def test_run_host_schedule_change_between_runs(gpu):
         assert_parity(out, O.dpd(x, taps, sched, period))
 
 
+@pytest.mark.parametrize("splits", [(5,), (5, 4), (1, 1, 7), (3, 3, 3)])
+def test_run_host_split_stream_equals_one_run(gpu, splits):
+    """Several df_dpd_run_host calls without a reset continue the FIR
+    history AND the schedule position, so a stream split at any block count
+    (not only at multiples of the schedule length) equals one oracle run."""
+    from paper_1611_03226_b200 import dpd
+    period, T = 128, 10
+    taps = O.random_taps(77, T)
+    sched = np.array([0x3FF, 0x001, 0x0F0, 0x206], np.uint16)  # length 4
+    blocks = sum(splits) + 2
+    x = O.synth_samples(period * blocks, 78)
+    want = O.dpd(x, taps, sched, period)
+    a = dpd.DpdActor(period, taps)
+    got = np.empty_like(x)
+    b0 = 0
+    for nb in list(splits) + [2]:
+        lo, hi = 2 * period * b0, 2 * period * (b0 + nb)
+        out = np.empty(hi - lo, np.float32)
+        a.run_host(np.ascontiguousarray(x[lo:hi]), out, sched)
+        got[lo:hi] = out
+        b0 += nb
+    a.check()
+    assert_parity(got, want)
+
+
 def test_gating_invariance_acceptance9(gpu):
     # proj/tests/acceptance.cpp:398-450: branch 7 toggled; inactive periods
     # must be bit-identical when its taps change.

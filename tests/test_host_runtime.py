@@ -17,6 +17,13 @@ def test_delayed_self_loop_is_legal():
     assert H.validate_demo(2) == 0
 
 
+def test_cycles_through_rate2_delay_channels_are_violations():
+    # A delay token covers one firing only at rate 1: a cycle whose delay
+    # channels all have rate > 1 blocks forever in the reference's read_start.
+    assert H.validate_demo(5) == 1
+    assert H.validate_demo(6) == 1
+
+
 def test_unknown_channel_is_build_error():
     assert H.validate_demo(3) == -1
     assert b"BuildError" in H.lib().dfh_last_error()

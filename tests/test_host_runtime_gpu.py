@@ -20,7 +20,7 @@ def test_dpd_network_equals_oracle(gpu, period, batch, blocks):
     taps = O.random_taps(41)
     sched = O.random_schedule(5, 42)
     sched[1] = 1  # a single-branch block (extension; the oracle accepts it)
-    got, ms, firings = H.dpd_run(x, taps, sched, period, batch)
+    got, ms, firings = H.dpd_run(x, taps, sched, period, batch, allow_single_branch=True)
     assert firings == blocks // batch
     np.testing.assert_array_equal(bits(got), bits(O.dpd(x, taps, sched, period)))
 
@@ -38,6 +38,11 @@ def test_dpd_network_rejects_bad_schedule(gpu):
         H.dpd_run(x, O.random_taps(1), [0x7FF], 64)  # branch 11 (check_config)
     with pytest.raises(H.HostRunError, match="invalid_argument"):
         H.dpd_run(x, O.random_taps(1), [3], 48)  # samples not a multiple of period
+    # k = 1 is outside the reference's [2,10] unless explicitly allowed
+    with pytest.raises(H.HostRunError, match=r"outside \[2,10\]"):
+        H.dpd_run(x, O.random_taps(1), [0x1], 64)
+    got, _, _ = H.dpd_run(x, O.random_taps(1), [0x1], 64, allow_single_branch=True)
+    np.testing.assert_array_equal(bits(got), bits(O.dpd(x, O.random_taps(1), [0x1], 64)))
 
 
 @pytest.mark.parametrize("rate", [1, 4, 7])
@@ -91,3 +96,15 @@ def test_mixed_network_cpu_actor_fault(gpu):
     rgb = O.synth_bytes(8 * w * h * 3, 3)
     with pytest.raises(H.HostRunError, match="ActorFault: actor 'census' faulted: census: injected fault"):
         H.motion_run_mixed(rgb, w, h, 32, 1, fail_at_firing=3)
+
+
+@pytest.mark.parametrize("rate", [1, 2, 3])
+@pytest.mark.parametrize("sink_first", [False, True])
+def test_delay_channel_orders_firings(gpu, rate, sink_first):
+    """A delay channel of rate r > 1 orders producer firing i before consumer
+    firing i (it needs r-1 of its tokens); only a rate-1 delay shifts by a
+    whole firing.  Declaring the sink first must not change the stream."""
+    firings = 7
+    got = H.delay_chain_run(rate, sink_first, firings)
+    want = np.concatenate([[np.uint64(2**64 - 1)], np.arange(1, firings * rate, dtype=np.uint64)])
+    np.testing.assert_array_equal(got, want)
