@@ -52,4 +52,19 @@ struct Params {
 NetworkGraph build_network(const Params& params);
 std::uint64_t source_firings(const Params& params);  // launches
 
+inline constexpr unsigned kMaxHistory = 31;  // FirState samples for up to 32 taps
+
+// The reference's own network shape (dpd.cpp:151-356: source, config,
+// dynamic split, ten dynamic branches, dynamic adder, sink; 56 channels of
+// one period per token) as DEVICE-RESIDENT actors: the run is one
+// persistent kernel, every split/branch/adder firing reads its control
+// token and dispatches its 0-or-1 port rates on the device through the
+// reference's control functions (model.hpp:103-108), and the branches keep
+// their FirState frozen while gated off.  Input and output spans are host
+// memory (staged to HBM by the source's init, back by the sink's finish);
+// params.batch is ignored (one block per firing, as the reference).  Needs
+// source_firing_limit = samples / period.  branch_ctas: CTAs per branch
+// actor (source, split, adder and sink get half).
+NetworkGraph build_reference_network(const Params& params, int device = 0, std::uint32_t branch_ctas = 8);
+
 }  // namespace df::dpd

@@ -2,16 +2,23 @@
 //
 // Same vocabulary and rules as the reference's dynflow model
 // (/root/reference/proj/include/dynflow/model.hpp:14-193): ChannelSpec,
-// PortSpec, ActorSpec, ActorBehavior, build_network, validate.  What
-// changes for GPU actors: channel storage lives in HBM (df_channel), a
-// firing ENQUEUES device work on the actor's stream, and a dynamic GPU
-// actor's control function runs on the device (it consumes its control
-// token from the device ring), so `ActorBehavior::control` is replaced by
-// `device_control = true`.
+// PortSpec, ActorSpec, ActorBehavior, FiringRates, build_network,
+// validate, control_dispatch.  What changes for GPU actors: channel storage
+// lives in HBM (df_channel) and control tokens are consumed on the device.
+// Two kinds of GPU actor exist:
+//   * device-resident actors (ActorBehavior::device): the actor fires inside
+//     the network's persistent kernel (df_net); a dynamic one keeps the
+//     reference's `control` function, which the runtime evaluates once per
+//     possible token value into a device table, so control_dispatch happens
+//     on the device per firing (0 or r per port, ControlError otherwise);
+//   * host-issued actors (ActorBehavior::fire): each firing enqueues device
+//     work on the actor's stream; a dynamic one (`device_control`) consumes
+//     its control tokens inside its own kernels (the fused DPD actor).
 #pragma once
 
 #include <cstddef>
 #include <cstdint>
+#include <cstring>
 #include <functional>
 #include <optional>
 #include <span>
@@ -117,19 +124,58 @@ class HostFiringContext {
   std::uint64_t firing_index_ = 0;
 };
 
-// model.hpp:103-108: mandatory fire; optional init / finish.  A GPU actor
-// sets `fire` (it enqueues device work); a CPU actor sets `host_fire`
-// instead (it computes on host spans, in stream order -- static rates
-// only).  A dynamic GPU actor sets device_control: its kernels consume one
-// control token per logical firing on the device (rates 0 or r decided
-// there).
+// model.hpp:89-97: rates of one firing of a dynamic actor, one entry per
+// regular port in declaration order, each 0 or the channel's rate.
+struct FiringRates {
+  std::vector<std::uint32_t> by_regular_port;
+  static FiringRates uniform(std::size_t port_count, std::uint32_t rate) {
+    FiringRates r;
+    r.by_regular_port.assign(port_count, rate);
+    return r;
+  }
+};
+
+// An actor that fires inside the device-resident network kernel: one of
+// the library's device actor kinds (DF_ACT_* in df_cuda.h) with its
+// parameters, run by `ctas` CTAs.
+struct DeviceActor {
+  int kind = 0;  // 0: not device-resident
+  std::vector<std::byte> params;
+  std::uint32_t ctas = 1;
+  template <typename P>
+  static DeviceActor of(int kind, const P& p, std::uint32_t ctas = 1) {
+    DeviceActor d;
+    d.kind = kind;
+    d.params.resize(sizeof(P));
+    std::memcpy(d.params.data(), &p, sizeof(P));
+    d.ctas = ctas;
+    return d;
+  }
+};
+
+// model.hpp:103-108: mandatory fire; optional init / control / finish.
+//   * fire       host-issued GPU actor: enqueues device work per firing;
+//   * host_fire  CPU actor: computes on host spans in stream order (static
+//                rates, host-issued networks);
+//   * device     device-resident GPU actor (see DeviceActor).
+// control (the reference's signature) is required for a dynamic
+// device-resident actor: it maps one control token to FiringRates and is
+// evaluated for every token value v < control_domain (v little-endian in
+// the token's bytes) into the device control table before the run; a
+// result that is not 0-or-r per port (or a throw) makes that token a
+// ControlError when a firing reads it.  device_control marks a host-issued
+// dynamic actor that consumes its control tokens inside its own kernels.
 struct ActorBehavior {
   std::function<void(FiringContext&)> fire;
   std::function<void(HostFiringContext&)> host_fire;
   std::function<void()> init;
+  std::function<FiringRates(std::span<const std::byte>)> control;
   std::function<void()> finish;
+  std::uint32_t control_domain = 1024;
   bool device_control = false;
+  DeviceActor device;
   bool is_host() const { return static_cast<bool>(host_fire); }
+  bool is_device_resident() const { return device.kind != 0; }
 };
 
 struct ActorSpec {
@@ -201,6 +247,12 @@ bool orders_same_firing(const ChannelSpec& spec);
 // nullopt when they form a cycle.  The static schedule issues firing i of
 // every actor in this order.
 std::optional<std::vector<std::size_t>> firing_order(const NetworkGraph& net);
+
+// model.cpp:240-265: runs the actor's control function on one token and
+// checks the result (one entry per regular port, each 0 or the attached
+// channel's rate); ControlError otherwise.  The device runtime evaluates
+// this per token value before a run (df_net_set_control_table).
+FiringRates control_dispatch(const NetworkGraph& net, std::size_t actor, std::span<const std::byte> control_token);
 
 // One "a -> b -> a" path per cyclic component of the graph of channels
 // selected by `edge` (validate()'s cycle findings).

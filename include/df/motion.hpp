@@ -30,6 +30,13 @@ struct Params {
 NetworkGraph build_network(const Params& params);
 std::uint64_t source_firings(const Params& params);
 
+// The reference's own network shape (motion.cpp:107-218: source -> gauss ->
+// cur + prev (delay channel, black initial frame) -> thres -> med -> sink,
+// rate r on every channel) as DEVICE-RESIDENT actors, each run by `ctas`
+// CTAs of one persistent kernel.  Gray input only (the reference's format);
+// host spans staged to HBM by the source's init / back by the sink's finish.
+NetworkGraph build_reference_network(const Params& params, int device = 0, std::uint32_t ctas = 16);
+
 // Heterogeneous network (CPU + GPU actors on shared device channels, the
 // paper's mixed mapping): source (H2D, RGB) -> gray (CPU actor: BT.601
 // integer luma) -> motion (GPU actor, gray input) -> census (CPU actor:

@@ -37,6 +37,9 @@ struct ExecutionConfig {
   int device = 0;
   std::optional<std::uint64_t> source_firing_limit;
   bool stats_enabled = true;
+  // Device-resident runs: the watchdog for any single channel wait (a
+  // deadlocked network ends in ActorFault instead of hanging the GPU).
+  double device_timeout_s = 30.0;
 };
 
 struct RunStats {
@@ -86,10 +89,14 @@ class RunAborted : public std::runtime_error {
   RunAborted() : std::runtime_error("run aborted") {}
 };
 
-// Validates, creates the device channels, runs init, issues
-// source_firing_limit firings of every actor (the network's actors fire in
-// lock step: every channel has the same rate at both ends), synchronizes,
-// runs finish, checks device-side errors and returns the stats.
+// Validates, creates the device channels and runs init, then either
+//   * (device-resident actors) runs the network as one persistent kernel:
+//     sources fire source_firing_limit times, every other actor until end
+//     of stream, with dynamic rates dispatched on the device per firing --
+//     the reference's run() semantics; or
+//   * (host-issued actors) issues source_firing_limit firings of every actor
+//     as a static schedule (the actors fire in lock step), synchronizes;
+// then runs finish, checks device-side errors and returns the stats.
 RunStats run(const NetworkGraph& net, const ExecutionConfig& cfg);
 
 // Throws the C++ exception matching a df_* status (DF_EINVAL ->

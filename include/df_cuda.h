@@ -42,7 +42,8 @@ extern "C" {
 #define DF_EABORTED 3  /* channel aborted               -> RunAborted */
 #define DF_ECUDA 4     /* CUDA runtime / launch failure */
 #define DF_ECONTROL 5  /* control token maps to an illegal rate -> ControlError */
-#define DF_EOS 6       /* read_start on a closed, drained channel (nullopt) */
+#define DF_EOS 6       /* read_start on a closed channel holding fewer than r
+                          tokens (nullopt, channel.cpp:114-140) */
 
 const char* df_last_error(void);
 int df_abi_version(void); /* bumps on any signature change */
@@ -116,9 +117,13 @@ size_t df_slot_read_first(uint32_t rate, int has_delay, unsigned phase);
 /* Stream-ordered host-side transfers for host-driven endpoints (source /
  * sink actors, tests).  *_start with n != token_rate -> DF_ELOGIC, as the
  * reference (channel.cpp:65-68).  A host-driven endpoint owns its phase, so
- * its region address is known without a device round trip; availability
- * is enforced on the device (a violation sets the sticky error word and is
- * reported by df_channel_stats / df_channel_check). */
+ * its region address is known without a device round trip.  Blocking is
+ * replaced by stream order: the host does not wait for tokens or room --
+ * availability and capacity are checked on the device, where a violation
+ * sets the sticky error word (df_channel_stats / df_channel_check).
+ * End of stream: read_start on a channel that has been closed (by
+ * df_channel_close or by the end of a device-resident run) synchronizes
+ * and returns DF_EOS when fewer than n tokens remain. */
 typedef struct df_region {
   void* dptr;          /* device address of the first token of the region */
   size_t first_slot;
@@ -273,6 +278,99 @@ int df_motion_median5(const uint8_t* in_dev, uint8_t* out_dev, unsigned w, unsig
                       void* stream);
 int df_motion_rgb_to_gray(const uint8_t* rgb_dev, uint8_t* gray_dev, size_t pixels,
                           void* stream);
+
+/* ---- device-resident networks (persistent actors) ----------------------
+ * Replaces the reference's thread-per-actor run (Run::execute / actor_main
+ * / fire_once, src/runtime.cpp:132-299) for networks whose actors all fire
+ * on the GPU.  ONE cooperative persistent kernel runs the whole network:
+ * each actor is a group of CTAs whose leader loops over the actor's
+ * firings exactly as fire_once does -- read one control token (dynamic
+ * actors) and dispatch it to per-port rates of 0 or r through the actor's
+ * control table (control_dispatch, src/model.cpp:240-265), wait by spinning
+ * on the HBM ring counters for r tokens on each active input and room for
+ * r on each active output (read_start / write_start), publish the regions
+ * to its CTAs, which fire, then commit outputs before inputs (write_end
+ * with the Fig. 2 phase-2 copy, read_end).  A source stops at its firing
+ * limit; an actor stops at end of stream on any input (read_start ->
+ * nullopt: closed and fewer than r tokens left), then closes its outputs
+ * and drains its inputs (src/runtime.cpp:206-231).  A fault (illegal
+ * control token -> DF_ECONTROL, watchdog -> DF_ETIMEOUT) or df_net_abort
+ * aborts every actor (RunAborted, src/channel.cpp:170-177).  No host round
+ * trip happens between firings; token counts never leave the device. */
+#define DF_ETIMEOUT 7 /* watchdog: an actor waited longer than the run's timeout */
+
+#define DF_ACT_DPD_SOURCE 1   /* interleaved complex f32 -> re, im planes (dpd.cpp:189-204) */
+#define DF_ACT_DPD_CONFIG 2   /* schedule[firing % len] -> every output (dpd.cpp:206-221) */
+#define DF_ACT_DPD_SPLIT 3    /* in re,im -> active branch pairs (dpd.cpp:225-256) */
+#define DF_ACT_DPD_BRANCH 4   /* poly_branch -> fir with frozen history (dpd.cpp:258-289) */
+#define DF_ACT_DPD_ADDER 5    /* +0.0f then active pairs ascending (dpd.cpp:293-331) */
+#define DF_ACT_DPD_SINK 6     /* re, im planes -> interleaved complex f32 (dpd.cpp:333-347) */
+#define DF_ACT_TEST_PRODUCE 7 /* splitmix64 token stream on output 0 (acceptance.cpp:62-66) */
+#define DF_ACT_TEST_CONSUME 8 /* checks that stream on input 0 */
+#define DF_ACT_FRAME_SOURCE 9 /* u8 frames -> output 0 (motion.cpp:123-129) */
+#define DF_ACT_GAUSS 10       /* gauss5x5, result to every output (motion.cpp:144-154) */
+#define DF_ACT_THRES 11       /* in0 prev, in1 cur -> thres_diff (motion.cpp:157-166) */
+#define DF_ACT_MEDIAN 12      /* median5 (motion.cpp:168-176) */
+#define DF_ACT_FRAME_SINK 13  /* input 0 -> u8 frames (motion.cpp:178-183) */
+
+/* Kind parameters (passed by value to df_net_add_actor).  Buffers are
+ * device pointers or mapped pinned host pointers (df_host_alloc memory is
+ * mapped; the actor then streams over PCIe). */
+typedef struct df_act_samples { /* DPD_SOURCE (read) / DPD_SINK (write) */
+  void* samples;                 /* interleaved complex f32, firing i = block i */
+  uint32_t period;
+} df_act_samples;
+typedef struct df_act_config { /* DPD_CONFIG */
+  const uint16_t* schedule;     /* device */
+  uint32_t len;
+} df_act_config;
+typedef struct df_act_branch { /* DPD_BRANCH */
+  uint32_t branch;              /* 1..10: poly order */
+  uint32_t taps_per_branch;     /* 1..32 */
+  const float* taps;            /* device, taps_per_branch complex */
+  float* state;                 /* device, taps_per_branch-1 complex FirState, x[-(j+1)] */
+  uint32_t period;
+} df_act_branch;
+typedef struct df_act_test { /* TEST_PRODUCE / TEST_CONSUME */
+  uint64_t seed;
+  uint64_t* counters;           /* device: [0] tokens produced / consumed, [1] mismatches */
+  uint32_t stall_mask;          /* leader pauses ~2 us before a firing when (hash & mask) == 0; 0 = never */
+  uint32_t skip_initial;        /* consumer: the first token is the channel's zero delay token */
+  uint64_t hold_ns;             /* pause before every firing (abort tests) */
+} df_act_test;
+typedef struct df_act_frames { /* FRAME_SOURCE (read) / FRAME_SINK (write) / GAUSS / THRES / MEDIAN */
+  void* frames;                 /* W*H bytes per token, firing i = tokens [i*r, (i+1)*r) */
+  uint32_t width, height;
+  uint8_t threshold;            /* THRES */
+} df_act_frames;
+
+typedef struct df_net df_net;
+int df_net_create(int device, df_net** net);
+int df_net_destroy(df_net* net);
+/* Adds an actor of `kind` run by `ctas` CTAs.  control: the control channel
+ * of a dynamic actor (NULL for static), inputs / outputs: regular ports in
+ * declaration order (at most 24 each).  firing_limit: a source's
+ * source_firing_limit (0 = stop only at end of stream).  Channels bound to
+ * a network are device-driven at both ends. */
+int df_net_add_actor(df_net* net, int kind, const void* params, size_t params_bytes, uint32_t ctas,
+                     df_channel* control, df_channel* const* inputs, size_t n_in, df_channel* const* outputs,
+                     size_t n_out, uint64_t firing_limit, int* index);
+/* The device form of ActorBehavior::control (model.hpp:103-108) for a
+ * dynamic actor: row v (v < domain, the control token read as a
+ * little-endian integer) = { bits of the active inputs, bits of the active
+ * outputs, 1 if legal }.  A token >= domain or an illegal row faults the
+ * actor with DF_ECONTROL (ControlError), recording the token value. */
+int df_net_set_control_table(df_net* net, int actor, const uint32_t* rows, uint32_t domain);
+/* Runs the network to completion: one cooperative kernel; synchronizes.
+ * timeout_s: watchdog for any single wait (<= 0: 30 s).  Returns DF_OK, or
+ * the first fault's code (see df_net_fault) / DF_EABORTED. */
+int df_net_run(df_net* net, double timeout_s);
+/* From any host thread while df_net_run blocks: aborts the run. */
+int df_net_abort(df_net* net);
+int df_net_fault(const df_net* net, int* actor, int* code, uint32_t* token);
+/* After a run: firings, and device time from the first firing's start to
+ * the actor's stop (RunStats::active_seconds, bench.cpp:346-347). */
+int df_net_actor_stats(const df_net* net, int actor, uint64_t* firings, double* active_ms);
 
 /* ---- multi-GPU halos (NVLink peer copies; no collectives) ---------------
  * No reference counterpart: dynflow is one CPU process.  These serve the

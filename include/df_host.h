@@ -36,6 +36,24 @@ int dfh_motion_run(int device, const uint8_t* in_host, uint8_t* out_host, uint64
                    unsigned height, int input_format, uint8_t threshold, uint32_t token_rate,
                    double* sink_active_ms, uint64_t* delay_tokens_written);
 
+/* The reference's own network shapes as DEVICE-RESIDENT actors, run as one
+ * persistent kernel (df::dpd / df::motion ::build_reference_network):
+ * DPD: 15 actors / 56 channels, split / branches / adder dynamic with their
+ * control tokens dispatched on the device per firing (0 or 1 per port);
+ * firings[15] receives each actor's firing count in declaration order
+ * (source, config, split, branch01..10, adder, sink), channel_tokens[56]
+ * each channel's tokens written (channel declaration order, dpd.cpp:
+ * 167-184).  Motion: 5 actors (source, gauss, thres, med, sink) with the
+ * delay channel gauss_thres_prev; gray frames; firings[5].  timeout_s is
+ * the device watchdog (a deadlock ends in ActorFault). */
+int dfh_dpd_run_resident(int device, const float* in_host, float* out_host, uint64_t samples, uint32_t period,
+                         uint32_t taps_per_branch, const float* taps, const uint16_t* schedule, size_t schedule_len,
+                         int allow_single_branch, uint32_t branch_ctas, double timeout_s, double* sink_active_ms,
+                         uint64_t* firings, uint64_t* channel_tokens);
+int dfh_motion_run_resident(int device, const uint8_t* in_host, uint8_t* out_host, uint64_t frames, unsigned width,
+                            unsigned height, uint8_t threshold, uint32_t token_rate, uint32_t ctas, double timeout_s,
+                            double* sink_active_ms, uint64_t* firings);
+
 /* Heterogeneous CPU + GPU network (df::motion::build_mixed_network):
  * RGB in; the gray conversion and a per-frame moving-pixel census run as
  * CPU actors, the motion chain as a GPU actor, all on device channels.

@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("DF_CUDA_LIB", os.path.join(HERE, "libdf_cuda.so"))
 HEADER_PATH = os.path.join(os.path.dirname(HERE), "include", "df_cuda.h")
 
-DF_OK, DF_EINVAL, DF_ELOGIC, DF_EABORTED, DF_ECUDA, DF_ECONTROL, DF_EOS = range(7)
+DF_OK, DF_EINVAL, DF_ELOGIC, DF_EABORTED, DF_ECUDA, DF_ECONTROL, DF_EOS, DF_ETIMEOUT = range(8)
 DF_MOTION_GRAY, DF_MOTION_RGB = 1, 3
 
 
@@ -44,8 +44,16 @@ class CudaError(DfError):
     pass
 
 
+class EndOfStream(DfError):
+    """DF_EOS -- read_start on a closed, drained channel (nullopt)."""
+
+
+class WatchdogTimeout(DfError):
+    """DF_ETIMEOUT -- a device-resident actor waited past the run's timeout."""
+
+
 _EXC = {DF_EINVAL: InvalidArgument, DF_ELOGIC: LogicError, DF_EABORTED: RunAborted,
-        DF_ECUDA: CudaError, DF_ECONTROL: ControlError}
+        DF_ECUDA: CudaError, DF_ECONTROL: ControlError, DF_EOS: EndOfStream, DF_ETIMEOUT: WatchdogTimeout}
 
 
 class DfChanStats(C.Structure):
@@ -139,6 +147,14 @@ _SIGS = {
     "df_ipc_get_handle": (_i, [_vp, _vp]),
     "df_ipc_open_handle": (_i, [_i, _vp, _P(_vp)]),
     "df_ipc_close_handle": (_i, [_vp]),
+    "df_net_create": (_i, [_i, _P(_vp)]),
+    "df_net_destroy": (_i, [_vp]),
+    "df_net_add_actor": (_i, [_vp, _i, _vp, _sz, _u32, _vp, _vp, _sz, _vp, _sz, _u64, _P(_i)]),
+    "df_net_set_control_table": (_i, [_vp, _i, _vp, _u32]),
+    "df_net_run": (_i, [_vp, C.c_double]),
+    "df_net_abort": (_i, [_vp]),
+    "df_net_fault": (_i, [_vp, _P(_i), _P(_i), _P(_u32)]),
+    "df_net_actor_stats": (_i, [_vp, _i, _P(_u64), _P(C.c_double)]),
     "df_fill_random_u8": (_i, [_vp, _sz, _u64, _vp]),
     "df_fill_random_pm1": (_i, [_vp, _sz, _u64, _vp]),
     "df_kernel_launches": (_u64, []),

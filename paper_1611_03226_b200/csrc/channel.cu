@@ -223,8 +223,20 @@ int df_channel_read_start(df_channel* ch, size_t n, df_region* region) {
   DF_REQUIRE(!ch->aborted, DF_EABORTED, "run aborted");
   DF_REQUIRE(n == ch->rate, DF_ELOGIC, "channel: read of %zu tokens, rate is %u", n, ch->rate);
   DF_REQUIRE(ch->read_serial == 0, DF_ELOGIC, "channel: read already outstanding");
-  DF_REQUIRE(ch->reader != Endpoint::device, DF_ELOGIC,
+  DF_REQUIRE(ch->reader != Endpoint::device || ch->closed_host, DF_ELOGIC,
              "channel: read endpoint is device-driven; host reads would race its phase");
+  if (ch->closed_host) {
+    // End of stream (channel.cpp:114-140: closed and fewer than n tokens ->
+    // nullopt).  Once closed the producer is done, so the stream-ordered
+    // state can be read after synchronizing.
+    DF_CHECK_CUDA(cudaSetDevice(ch->device));
+    DF_CHECK_CUDA(cudaDeviceSynchronize());
+    DevChanState st;
+    DF_CHECK_CUDA(cudaMemcpy(&st, ch->state, sizeof st, cudaMemcpyDeviceToHost));
+    if (st.available < n) return set_error(DF_EOS, "channel: end of stream (closed, %llu < %zu tokens left)",
+                                           (unsigned long long)st.available, n);
+    ch->host_read_phase = st.read_phase;  // a device reader may have advanced it
+  }
   ch->reader = Endpoint::host;
   const size_t slot = chan_read_slot(ch->rate, ch->has_delay, ch->host_read_phase);
   region->first_slot = slot;

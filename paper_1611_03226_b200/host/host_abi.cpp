@@ -98,6 +98,60 @@ int dfh_motion_run(int device, const uint8_t* in_host, uint8_t* out_host, uint64
   });
 }
 
+int dfh_dpd_run_resident(int device, const float* in_host, float* out_host, uint64_t samples, uint32_t period,
+                         uint32_t T, const float* taps, const uint16_t* schedule, size_t schedule_len,
+                         int allow_single_branch, uint32_t branch_ctas, double timeout_s, double* sink_active_ms,
+                         uint64_t* firings, uint64_t* channel_tokens) {
+  return guarded([&] {
+    df::dpd::Params p;
+    p.period = period;
+    p.samples = samples;
+    p.taps_per_branch = T;
+    p.taps.resize(std::size_t(10) * T);
+    for (std::size_t i = 0; i < p.taps.size(); ++i) p.taps[i] = {taps[2 * i], taps[2 * i + 1]};
+    for (size_t i = 0; i < schedule_len; ++i) p.schedule.push_back({schedule[i]});
+    p.allow_single_branch = allow_single_branch != 0;
+    p.input = {reinterpret_cast<const std::complex<float>*>(in_host), samples};
+    p.output = {reinterpret_cast<std::complex<float>*>(out_host), samples};
+    df::NetworkGraph net = df::dpd::build_reference_network(p, device, branch_ctas);
+    df::ExecutionConfig cfg;
+    cfg.device = device;
+    cfg.source_firing_limit = samples / period;
+    cfg.device_timeout_s = timeout_s;
+    df::RunStats st = df::run(net, cfg);
+    if (sink_active_ms) *sink_active_ms = st.actor("sink").active_ms;
+    if (firings)
+      for (std::size_t a = 0; a < st.actors.size(); ++a) firings[a] = st.actors[a].firings;
+    if (channel_tokens)
+      for (std::size_t c = 0; c < st.channels.size(); ++c) channel_tokens[c] = st.channels[c].tokens_written;
+  });
+}
+
+int dfh_motion_run_resident(int device, const uint8_t* in_host, uint8_t* out_host, uint64_t frames, unsigned width,
+                            unsigned height, uint8_t threshold, uint32_t rate, uint32_t ctas, double timeout_s,
+                            double* sink_active_ms, uint64_t* firings) {
+  return guarded([&] {
+    df::motion::Params p;
+    p.width = width;
+    p.height = height;
+    p.threshold = threshold;
+    p.token_rate = rate;
+    p.frames = frames;
+    const std::size_t px = std::size_t(width) * height;
+    p.input = {in_host, frames * px};
+    p.output = {out_host, frames * px};
+    df::NetworkGraph net = df::motion::build_reference_network(p, device, ctas);
+    df::ExecutionConfig cfg;
+    cfg.device = device;
+    cfg.source_firing_limit = frames / rate;
+    cfg.device_timeout_s = timeout_s;
+    df::RunStats st = df::run(net, cfg);
+    if (sink_active_ms) *sink_active_ms = st.actor("sink").active_ms;
+    if (firings)
+      for (std::size_t a = 0; a < st.actors.size(); ++a) firings[a] = st.actors[a].firings;
+  });
+}
+
 int dfh_motion_run_mixed(int device, const uint8_t* rgb_host, uint8_t* out_host, uint64_t frames, unsigned width,
                          unsigned height, uint8_t threshold, uint32_t rate, uint32_t* counts,
                          int64_t fail_at_firing, double* sink_active_ms) {

@@ -128,6 +128,137 @@ void fire_host_actor(ActorRun& r, std::uint64_t firing, HostFaults& faults, std:
   for (std::size_t k = 0; k < nin; ++k) check(df_channel_read_end(r.ctx.input(k), &rin[k], r.stream));
 }
 
+// Device-resident run: every actor fires inside one persistent kernel
+// (df_net, csrc/netrt.cu).  The host builds the channels, registers each
+// actor with its kind, ports and firing limit, turns each dynamic actor's
+// `control` into a device table (control_dispatch per token value), runs
+// the kernel to completion and maps a device fault back to ActorFault.
+RunStats run_device(const NetworkGraph& net, const ExecutionConfig& cfg, std::chrono::steady_clock::time_point t0) {
+  check(df_set_device(cfg.device));
+  std::vector<df_channel*> chans(net.channels().size(), nullptr);
+  df_net* dn = nullptr;
+  auto cleanup = [&]() {
+    df_net_destroy(dn);
+    for (df_channel* c : chans) df_channel_destroy(c);
+  };
+  // control_dispatch failures per (actor, token value), for the fault text.
+  std::vector<std::vector<std::string>> control_errors(net.actors().size());
+  RunStats stats;
+  try {
+    for (std::size_t c = 0; c < chans.size(); ++c) {
+      const ChannelSpec& s = net.channels()[c];
+      check(df_channel_create(cfg.device, s.token_size, s.token_rate, s.has_delay,
+                              s.initial_token_value.empty() ? nullptr : s.initial_token_value.data(), &chans[c]));
+    }
+    check(df_net_create(cfg.device, &dn));
+    for (std::size_t a = 0; a < net.actors().size(); ++a) {
+      const ActorSpec& spec = net.actors()[a];
+      std::vector<df_channel*> in, out;
+      std::vector<std::pair<bool, std::uint32_t>> slot;  // regular port k -> (is input, bit)
+      df_channel* ctrl = nullptr;
+      for (const PortSpec& port : spec.ports) {
+        df_channel* ch = chans[net.channel_index(port.channel_id)];
+        if (port.kind == PortKind::control) {
+          ctrl = ch;
+        } else if (port.direction == PortDirection::input) {
+          slot.push_back({true, static_cast<std::uint32_t>(in.size())});
+          in.push_back(ch);
+        } else {
+          slot.push_back({false, static_cast<std::uint32_t>(out.size())});
+          out.push_back(ch);
+        }
+      }
+      std::uint64_t limit = 0;
+      if (in.empty() && !ctrl) {  // a source (runtime.cpp:105-107: no input, no control port)
+        if (!cfg.source_firing_limit)
+          throw std::invalid_argument("device-resident source '" + spec.id + "' needs a source_firing_limit");
+        limit = *cfg.source_firing_limit;
+        if (limit == 0) limit = ~std::uint64_t(0) >> 1;  // fires never; closes at once
+      }
+      const DeviceActor& d = spec.behavior.device;
+      int index = -1;
+      check(df_net_add_actor(dn, d.kind, d.params.empty() ? nullptr : d.params.data(), d.params.size(), d.ctas, ctrl,
+                             in.data(), in.size(), out.data(), out.size(), limit, &index));
+      if (ctrl) {
+        const std::size_t tsize = df_channel_token_size(ctrl);
+        std::uint64_t domain = spec.behavior.control_domain;
+        if (tsize < 4) domain = std::min<std::uint64_t>(domain, std::uint64_t(1) << (8 * tsize));
+        std::vector<std::uint32_t> rows(3 * domain, 0);
+        control_errors[a].assign(domain, {});
+        std::vector<std::byte> token(tsize, std::byte{0});
+        for (std::uint64_t v = 0; v < domain; ++v) {
+          for (std::size_t b = 0; b < tsize && b < 4; ++b) token[b] = static_cast<std::byte>((v >> (8 * b)) & 0xFF);
+          try {
+            const FiringRates r = control_dispatch(net, a, token);
+            for (std::size_t k = 0; k < slot.size(); ++k)
+              if (r.by_regular_port[k]) rows[3 * v + (slot[k].first ? 0 : 1)] |= 1u << slot[k].second;
+            rows[3 * v + 2] = 1;
+          } catch (const std::exception& e) {
+            control_errors[a][v] = e.what();
+          }
+        }
+        check(df_net_set_control_table(dn, index, rows.data(), static_cast<std::uint32_t>(domain)));
+      }
+    }
+  } catch (...) {
+    cleanup();
+    throw;
+  }
+  std::string fault_actor;
+  try {
+    for (const ActorSpec& spec : net.actors()) {
+      fault_actor = spec.id;
+      if (spec.behavior.init) spec.behavior.init();
+    }
+    fault_actor.clear();
+    const int rc = df_net_run(dn, cfg.device_timeout_s);
+    if (rc != DF_OK) {
+      const std::string detail = df_last_error();
+      int who = -1, code = 0;
+      std::uint32_t token = 0;
+      df_net_fault(dn, &who, &code, &token);
+      if (rc == DF_EABORTED || who < 0) throw_status(rc);
+      fault_actor = net.actors()[who].id;
+      if (code == DF_ECONTROL) {
+        const auto& errs = control_errors[who];
+        throw ControlError(token < errs.size() && !errs[token].empty()
+                               ? errs[token]
+                               : "actor '" + fault_actor + "': control token " + std::to_string(token) +
+                                     " is outside the control domain");
+      }
+      throw std::runtime_error(detail);
+    }
+    for (const ActorSpec& spec : net.actors()) {
+      fault_actor = spec.id;
+      if (spec.behavior.finish) spec.behavior.finish();
+    }
+    fault_actor.clear();
+  } catch (const RunAborted&) {
+    cleanup();
+    throw;
+  } catch (const std::exception& e) {
+    const std::string who = fault_actor;
+    cleanup();
+    if (!who.empty()) throw ActorFault(who, e.what());
+    throw;
+  }
+  for (std::size_t a = 0; a < net.actors().size(); ++a) {
+    std::uint64_t firings = 0;
+    double ms = 0.0;
+    df_net_actor_stats(dn, static_cast<int>(a), &firings, &ms);
+    stats.actors.push_back({net.actors()[a].id, firings, ms});
+  }
+  if (cfg.stats_enabled)
+    for (std::size_t c = 0; c < chans.size(); ++c) {
+      df_chan_stats st{};
+      if (df_channel_stats(chans[c], &st) == DF_OK)
+        stats.channels.push_back({net.channels()[c].id, st.tokens_written, st.tokens_read, st.tokens_available});
+    }
+  cleanup();
+  stats.wall = std::chrono::steady_clock::now() - t0;
+  return stats;
+}
+
 }  // namespace
 
 RunStats run(const NetworkGraph& net, const ExecutionConfig& cfg) {
@@ -139,6 +270,7 @@ RunStats run(const NetworkGraph& net, const ExecutionConfig& cfg) {
     throw ValidationError(msg.str(), std::move(violations));
   }
   const auto t0 = std::chrono::steady_clock::now();
+  if (!net.actors().empty() && net.actors().front().behavior.is_device_resident()) return run_device(net, cfg, t0);
   check(df_set_device(cfg.device));
 
   // Device channels (Eq. 1 storage + control block in HBM).

@@ -33,6 +33,12 @@ def lib():
         L.dfh_motion_run_mixed.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint, C.c_uint,
                                            C.c_uint8, C.c_uint32, C.c_void_p, C.c_int64, C.POINTER(C.c_double)]
         L.dfh_validate_demo.argtypes = [C.c_int]
+        L.dfh_dpd_run_resident.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32,
+                                           C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, C.c_uint32, C.c_double,
+                                           C.POINTER(C.c_double), C.c_void_p, C.c_void_p]
+        L.dfh_motion_run_resident.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint, C.c_uint,
+                                              C.c_uint8, C.c_uint32, C.c_uint32, C.c_double,
+                                              C.POINTER(C.c_double), C.c_void_p]
         L.dfh_delay_chain_run.argtypes = [C.c_int, C.c_uint32, C.c_int, C.c_uint64, C.c_void_p]
         L.dfh_memory.argtypes = [C.c_int, C.c_uint, C.c_uint, C.c_uint32, C.c_uint32, C.c_int,
                                  C.POINTER(C.c_uint64)]
@@ -110,3 +116,43 @@ def delay_chain_run(rate: int, sink_first: bool, firings: int, device: int = 0) 
     out = np.zeros(firings * rate, np.uint64)
     _check(lib().dfh_delay_chain_run(device, rate, int(sink_first), firings, out.ctypes.data_as(C.c_void_p)))
     return out
+
+
+DPD_ACTORS = ["source", "config", "split"] + [f"branch{b:02d}" for b in range(1, 11)] + ["adder", "sink"]
+MOTION_ACTORS = ["source", "gauss", "thres", "med", "sink"]
+
+
+def dpd_run_resident(inp: np.ndarray, taps: np.ndarray, schedule, period: int, device: int = 0,
+                     allow_single_branch: bool = False, branch_ctas: int = 8, timeout_s: float = 30.0):
+    """The reference's 15-actor DPD network as device-resident actors (one
+    persistent kernel); returns (output, sink_active_ms, {actor: firings},
+    channel tokens written [56])."""
+    inp = np.ascontiguousarray(inp, np.float32).reshape(-1)
+    taps = np.ascontiguousarray(taps, np.float32)
+    T = taps.shape[1]
+    sched = np.ascontiguousarray(np.asarray(schedule, np.uint16))
+    out = np.empty_like(inp)
+    ms = C.c_double(0)
+    fir = np.zeros(len(DPD_ACTORS), np.uint64)
+    tok = np.zeros(56, np.uint64)
+    _check(lib().dfh_dpd_run_resident(device, inp.ctypes.data_as(C.c_void_p), out.ctypes.data_as(C.c_void_p),
+                                      inp.size // 2, period, T, taps.ctypes.data_as(C.c_void_p),
+                                      sched.ctypes.data_as(C.c_void_p), sched.size, int(allow_single_branch),
+                                      branch_ctas, timeout_s, C.byref(ms), fir.ctypes.data_as(C.c_void_p),
+                                      tok.ctypes.data_as(C.c_void_p)))
+    return out, ms.value, dict(zip(DPD_ACTORS, fir.tolist())), tok
+
+
+def motion_run_resident(frames: np.ndarray, width: int, height: int, threshold: int = 32, rate: int = 1,
+                        device: int = 0, ctas: int = 16, timeout_s: float = 30.0):
+    """The reference's 5-actor motion network (gauss_thres_prev delay channel)
+    as device-resident actors; returns (masks, sink_active_ms, {actor: firings})."""
+    frames = np.ascontiguousarray(frames, np.uint8).reshape(-1)
+    n = frames.size // (width * height)
+    out = np.empty(n * width * height, np.uint8)
+    ms = C.c_double(0)
+    fir = np.zeros(5, np.uint64)
+    _check(lib().dfh_motion_run_resident(device, frames.ctypes.data_as(C.c_void_p), out.ctypes.data_as(C.c_void_p),
+                                         n, width, height, threshold, rate, ctas, timeout_s, C.byref(ms),
+                                         fir.ctypes.data_as(C.c_void_p)))
+    return out, ms.value, dict(zip(MOTION_ACTORS, fir.tolist()))

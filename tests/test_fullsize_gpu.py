@@ -55,8 +55,9 @@ def _dpd_host(x, taps, sched, period, splits):
     s0 = 0
     for nb in splits:
         lo, hi = 2 * s0 * period, 2 * (s0 + nb) * period
-        # the schedule cycles per block from the stream start (dpd.cpp:208)
-        a.run_host(x[lo:hi], out[lo:hi], np.roll(sched, -(s0 % len(sched))))
+        # the schedule cycles per block from the stream start (dpd.cpp:208);
+        # run_host continues it from the blocks earlier calls fired
+        a.run_host(x[lo:hi], out[lo:hi], sched)
         s0 += nb
     a.check()
     return out
