@@ -116,6 +116,18 @@ __device__ void raise_fault(NetCtl* ctl, int actor, unsigned code, unsigned toke
   atomicExch(&ctl->abort, 1u);
 }
 
+// Is the run aborted (a device fault, or df_net_abort from the host)?  A
+// host abort is promoted to the device word so every actor sees it.
+__device__ bool aborted_now(NetCtl* ctl) {
+  if (*(volatile unsigned*)&ctl->abort) return true;
+  if (*ctl->host_abort) {
+    atomicCAS(&ctl->fault_code, 0u, (unsigned)DF_EABORTED);
+    atomicExch(&ctl->abort, 1u);
+    return true;
+  }
+  return false;
+}
+
 struct Spin {
   unsigned long long t0 = 0;
   unsigned n = 0;
@@ -202,6 +214,10 @@ __device__ bool leader_prepare(const ActorDesc& A, int a, ActorRt* rt, NetCtl* c
   const unsigned long long i = rt->firings;
   bool stop = false;
   if (A.limit && i >= A.limit) stop = true;  // source firing limit (runtime.cpp:217-219)
+  if (!stop && aborted_now(ctl)) {  // checked once per firing, not only inside waits
+    stop = true;
+    *aborted = true;
+  }
   unsigned in_on = A.n_in >= 32 ? 0xffffffffu : (1u << A.n_in) - 1;
   unsigned out_on = A.n_out >= 32 ? 0xffffffffu : (1u << A.n_out) - 1;
   if (!stop && A.kind == DF_ACT_TEST_PRODUCE) {  // scripted stalls (concurrency tests)
@@ -210,7 +226,11 @@ __device__ bool leader_prepare(const ActorDesc& A, int a, ActorRt* rt, NetCtl* c
     if (P.stall_mask && (mix64(P.seed ^ (i * 0x51ed27ull)) & P.stall_mask) == 0) pause += 2000;
     const unsigned long long t0 = now_ns();
     while (pause && now_ns() - t0 < pause) {
-      if (*(volatile unsigned*)&ctl->abort || *ctl->host_abort) break;
+      if (aborted_now(ctl)) {
+        stop = true;
+        *aborted = true;
+        break;
+      }
       __nanosleep(1000);
     }
   }
