@@ -214,7 +214,7 @@ def bench_motion_ours(args, p, rank, world, local):
         torch.cuda.synchronize()
         dist.barrier()  # every shard is filled before a neighbour maps it
         if HALO == "ipc":
-            peer = shard.PeerBuffer(inp.data_ptr(), local, rank, world)
+            peer = shard.PeerBuffer(inp.data_ptr(), local, rank, world, lower="prev")
             if rank > 0:
                 pipe = HaloPipe(torch, stream, local, peer.device)
     nstep = [0]
@@ -391,8 +391,10 @@ def bench_dpd_ours(args, p, rank, world, local):
     taps = np.random.default_rng(808).uniform(-0.5, 0.5, size=(10, T, 2)).astype(np.float32)
     actor = dpd.DpdActor(period, taps, device=local)
     sched_np = np.ascontiguousarray(sched)
-    _lib.call("df_dpd_config_tokens", local, sched_np.ctypes.data_as(C.c_void_p), sched_np.size, 0, blocks,
-              C.c_void_p(ctrl.data_ptr()), sh)
+    # Rank r holds global blocks [r*blocks, (r+1)*blocks): its control tokens
+    # continue the global schedule (dpd.cpp:208 schedule[firing % len]).
+    _lib.call("df_dpd_config_tokens", local, sched_np.ctypes.data_as(C.c_void_p), sched_np.size, rank * blocks,
+              blocks, C.c_void_p(ctrl.data_ptr()), sh)
 
     # Block-range shard of a weak-scaled stream: rank r holds blocks
     # [r*blocks, (r+1)*blocks).  FIR-history halo: for each branch, the last
@@ -404,9 +406,9 @@ def bench_dpd_ours(args, p, rank, world, local):
     tails = torch.zeros(10 * H1 * 2, dtype=torch.float32, device=dev)
     halo = torch.zeros_like(tails)
     tail_src = []
-    for b in range(1, 11):
-        hb = shard.dpd_halo_block(sched, blocks, b)  # last active block of this rank (local index)
-        tail_src.append(hb)
+    for b in range(1, 11):  # last active block of this rank's range (local index), for the P2P variant
+        hb = shard.dpd_halo_block(sched, (rank + 1) * blocks, b)
+        tail_src.append(hb - rank * blocks if hb is not None and hb >= rank * blocks else None)
     peer = None
     if world > 1:
         torch.cuda.synchronize()
@@ -418,8 +420,13 @@ def bench_dpd_ours(args, p, rank, world, local):
     # extra launch; only the block-start tiles that need a tail touch it.
     tail_ptrs = None
     if peer is not None and rank > 0:
-        tail_ptrs = (C.c_void_p * 10)(*[C.c_void_p(peer.ptr + 8 * ((hb + 1) * period - H1)) if hb is not None
-                                        else None for hb in tail_src])
+        # The global stream is the ranks' shards back to back (the schedule
+        # cycling over global block indices), so each branch's halo is
+        # the tail of its last active block before this shard, on whichever
+        # lower rank holds it (shard.dpd_halo_tails).
+        ranges = [(r * N, (r + 1) * N) for r in range(world)]
+        tails_g = shard.dpd_halo_tails(sched, ranges, period, T, rank, peer.peers)  # global block indices
+        tail_ptrs = (C.c_void_p * 10)(*[C.c_void_p(t) if t is not None else None for t in tails_g])
 
     def step(ev0=None, ev1=None):
         sh = C.c_void_p(torch.cuda.current_stream().cuda_stream)  # the capture stream inside a graph

@@ -294,6 +294,139 @@ void orc_motion_rgb(const uint8_t* rgb, size_t count, unsigned w, unsigned h, ui
 }
 
 /* ------------------------------------------------------------------------
+ * Multi-threaded drivers of the restatements above (whole-output parity at
+ * BASELINE sizes).  They split the stream into block / frame ranges and
+ * give each range exactly the state the serial run has at its start, so
+ * the result is bit-identical to orc_dpd / orc_motion_rgb / orc_motion_gray
+ * (checked against them in tests/test_oracle.py):
+ *   DPD     branch b's FIR history at block p0 is the poly of the last T-1
+ *           samples of b's ACTIVE input stream before p0 (fir10's state
+ *           update, dpd.cpp:108-120; poly_branch is memoryless), zeros if
+ *           fewer were seen;
+ *   motion  the delay token of frame f0 is gauss(gray(f0 - 1)) (black for
+ *           frame 0, motion.cpp:239-251).
+ * ---------------------------------------------------------------------- */
+#include <pthread.h>
+
+typedef struct {
+  const float* in; const float* taps; unsigned T; const uint16_t* sched; size_t len;
+  uint32_t period; size_t p0, p1; float* out;
+} dpd_job;
+
+static void* dpd_range(void* arg) {
+  const dpd_job* j = (const dpd_job*)arg;
+  const uint32_t period = j->period;
+  const unsigned H1 = j->T - 1;
+  float* state = (float*)calloc((size_t)10 * 128, sizeof(float));
+  float* bre = (float*)malloc(sizeof(float) * period);
+  float* bim = (float*)malloc(sizeof(float) * period);
+  float* pre = (float*)malloc(sizeof(float) * period);
+  float* pim = (float*)malloc(sizeof(float) * period);
+  float* fre = (float*)malloc(sizeof(float) * period);
+  float* fim = (float*)malloc(sizeof(float) * period);
+  float* are = (float*)malloc(sizeof(float) * period);
+  float* aim = (float*)malloc(sizeof(float) * period);
+  /* History at p0: walk back over each branch's active blocks. */
+  for (unsigned b = 1; b <= 10; ++b) {
+    float* st = state + (size_t)(b - 1) * 128;
+    unsigned got = 0;
+    for (size_t q = j->p0; q-- > 0 && got < H1;) {
+      if (!((j->sched[q % j->len] >> (b - 1)) & 1u)) continue;
+      for (size_t i = period; i-- > 0 && got < H1; ++got) {
+        float re, im;
+        orc_poly_branch(b, &j->in[2 * (q * period + i)], &j->in[2 * (q * period + i) + 1], 1, &re, &im);
+        st[got] = re;
+        st[64 + got] = im;
+      }
+    }
+  }
+  for (size_t p = j->p0; p < j->p1; ++p) {  /* the serial loop of orc_dpd, dpd.cpp:370-389 */
+    const uint16_t cfg = j->sched[p % j->len];
+    for (size_t i = 0; i < period; ++i) {
+      bre[i] = j->in[2 * (p * period + i)];
+      bim[i] = j->in[2 * (p * period + i) + 1];
+      are[i] = 0.0f;
+      aim[i] = 0.0f;
+    }
+    for (unsigned b = 1; b <= 10; ++b) {
+      if (!((cfg >> (b - 1)) & 1u)) continue;
+      orc_poly_branch(b, bre, bim, period, pre, pim);
+      float* st = state + (size_t)(b - 1) * 128;
+      orc_fir(j->T, j->taps + 2 * (size_t)(b - 1) * j->T, st, st + 64, pre, pim, period, fre, fim);
+      for (size_t i = 0; i < period; ++i) {
+        are[i] += fre[i];
+        aim[i] += fim[i];
+      }
+    }
+    for (size_t i = 0; i < period; ++i) {
+      j->out[2 * (p * period + i)] = are[i];
+      j->out[2 * (p * period + i) + 1] = aim[i];
+    }
+  }
+  free(state); free(bre); free(bim); free(pre); free(pim);
+  free(fre); free(fim); free(are); free(aim);
+  return NULL;
+}
+
+int orc_dpd_mt(const float* in, size_t samples, const float* taps, unsigned T, const uint16_t* schedule,
+               size_t schedule_len, uint32_t period, float* out, unsigned threads) {
+  if (schedule_len == 0 || period == 0 || samples % period != 0) return -1;
+  if (T < 1 || T > 64) return -1;
+  const size_t periods = samples / period;
+  if (threads < 1) threads = 1;
+  if (threads > periods) threads = periods ? (unsigned)periods : 1;
+  pthread_t* tid = (pthread_t*)malloc(sizeof(pthread_t) * threads);
+  dpd_job* jobs = (dpd_job*)malloc(sizeof(dpd_job) * threads);
+  for (unsigned t = 0; t < threads; ++t) {
+    dpd_job jb = {in, taps, T, schedule, schedule_len, period, periods * t / threads, periods * (t + 1) / threads, out};
+    jobs[t] = jb;
+    pthread_create(&tid[t], NULL, dpd_range, &jobs[t]);
+  }
+  for (unsigned t = 0; t < threads; ++t) pthread_join(tid[t], NULL);
+  free(tid); free(jobs);
+  return 0;
+}
+
+typedef struct {
+  const uint8_t* frames; size_t f0, f1; unsigned w, h; uint8_t thr; int rgb; const uint8_t* prev0; uint8_t* out;
+} motion_job;
+
+static void* motion_range(void* arg) {
+  const motion_job* j = (const motion_job*)arg;
+  const size_t px = (size_t)j->w * j->h, fb = px * (j->rgb ? 3 : 1);
+  const uint8_t* prev = j->f0 ? j->frames + (j->f0 - 1) * fb : j->prev0;
+  if (j->rgb) {
+    orc_motion_rgb(j->frames + j->f0 * fb, j->f1 - j->f0, j->w, j->h, j->thr, prev, j->out + j->f0 * px);
+  } else if (!prev) {
+    orc_motion_gray(j->frames + j->f0 * fb, j->f1 - j->f0, j->w, j->h, j->thr, j->out + j->f0 * px);
+  } else {  /* gray with a halo frame: run from f0 - 1 and drop its mask */
+    uint8_t* tmp = (uint8_t*)malloc((j->f1 - j->f0 + 1) * px);
+    orc_motion_gray(prev, j->f1 - j->f0 + 1, j->w, j->h, j->thr, tmp);
+    memcpy(j->out + j->f0 * px, tmp + px, (j->f1 - j->f0) * px);
+    free(tmp);
+  }
+  return NULL;
+}
+
+/* fmt 1 = gray, 3 = RGB; prev0: the halo frame before frame 0 (RGB only),
+ * or NULL for the black initial token. */
+void orc_motion_mt(const uint8_t* frames, size_t count, unsigned w, unsigned h, int fmt, uint8_t threshold,
+                   const uint8_t* prev0, uint8_t* out, unsigned threads) {
+  if (threads < 1) threads = 1;
+  if (threads > count) threads = count ? (unsigned)count : 1;
+  pthread_t* tid = (pthread_t*)malloc(sizeof(pthread_t) * threads);
+  motion_job* jobs = (motion_job*)malloc(sizeof(motion_job) * threads);
+  for (unsigned t = 0; t < threads; ++t) {
+    motion_job jb = {frames, count * t / threads, count * (t + 1) / threads, w, h, threshold, fmt == 3,
+                     fmt == 3 ? prev0 : NULL, out};
+    jobs[t] = jb;
+    pthread_create(&tid[t], NULL, motion_range, &jobs[t]);
+  }
+  for (unsigned t = 0; t < threads; ++t) pthread_join(tid[t], NULL);
+  free(tid); free(jobs);
+}
+
+/* ------------------------------------------------------------------------
  * Channel slot walk (channel.cpp:9-32) and comparator (bench.cpp:307-326)
  * ---------------------------------------------------------------------- */
 size_t orc_capacity_tokens(uint32_t r, int has_delay) {

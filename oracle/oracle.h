@@ -74,6 +74,18 @@ void orc_rgb_to_gray(const uint8_t* rgb, size_t pixels, uint8_t* gray);
 void orc_motion_rgb(const uint8_t* rgb, size_t count, unsigned w, unsigned h, uint8_t threshold,
                     const uint8_t* prev_rgb, uint8_t* out);
 
+/* ---- multi-threaded drivers (bit-identical to the serial functions) ----
+ * orc_dpd_mt: block ranges per thread, each starting from branch b's FIR
+ * history = poly of the last T-1 samples of b's active stream before the
+ * range (dpd.cpp:108-120).  orc_motion_mt: frame ranges, each starting
+ * from gauss(gray(frame f0-1)); fmt 1 gray / 3 RGB; prev0 = RGB halo frame
+ * before frame 0 or NULL (black). */
+int orc_dpd_mt(const float* in_interleaved, size_t samples, const float* taps_interleaved, unsigned T,
+               const uint16_t* schedule, size_t schedule_len, uint32_t period, float* out_interleaved,
+               unsigned threads);
+void orc_motion_mt(const uint8_t* frames, size_t count, unsigned w, unsigned h, int fmt, uint8_t threshold,
+                   const uint8_t* prev0, uint8_t* out, unsigned threads);
+
 /* ---- channel slot walk (proj/src/channel.cpp:9-32) ---------------------- */
 size_t orc_capacity_tokens(uint32_t rate, int has_delay);
 size_t orc_write_slot(uint32_t rate, int has_delay, unsigned phase);

@@ -52,6 +52,11 @@ def port():
         lib.orc_dpd.restype = C.c_int
         lib.orc_dpd.argtypes = [C.c_void_p, C.c_size_t, C.c_void_p, C.c_uint, C.c_void_p, C.c_size_t,
                                 C.c_uint32, C.c_void_p]
+        lib.orc_dpd_mt.restype = C.c_int
+        lib.orc_dpd_mt.argtypes = [C.c_void_p, C.c_size_t, C.c_void_p, C.c_uint, C.c_void_p, C.c_size_t,
+                                   C.c_uint32, C.c_void_p, C.c_uint]
+        lib.orc_motion_mt.argtypes = [C.c_void_p, C.c_size_t, C.c_uint, C.c_uint, C.c_int, C.c_uint8, C.c_void_p,
+                                      C.c_void_p, C.c_uint]
         lib.orc_compare_samples.restype = C.c_int64
         lib.orc_compare_samples.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_double, _dp]
         for name in ("orc_capacity_tokens", "orc_write_slot", "orc_read_slot"):
@@ -161,6 +166,35 @@ def dpd(inp: np.ndarray, taps: np.ndarray, schedule, period: int) -> np.ndarray:
     rc = port().orc_dpd(_ptr(inp), n, _ptr(taps), T, _ptr(sched), sched.size, period, _ptr(out))
     if rc != 0:
         raise ValueError("oracle_dpd: bad schedule or period")
+    return out
+
+
+def _threads(threads):
+    return threads or max(1, len(os.sched_getaffinity(0)))
+
+
+def dpd_mt(inp: np.ndarray, taps: np.ndarray, schedule, period: int, threads: int | None = None) -> np.ndarray:
+    """oracle_dpd over block ranges in parallel; bit-identical to dpd()."""
+    inp = np.ascontiguousarray(inp, np.float32).reshape(-1)
+    taps = np.ascontiguousarray(taps, np.float32)
+    sched = np.ascontiguousarray(np.asarray(schedule, np.uint16))
+    out = np.empty_like(inp)
+    rc = port().orc_dpd_mt(_ptr(inp), inp.size // 2, _ptr(taps), taps.shape[1], _ptr(sched), sched.size, period,
+                           _ptr(out), _threads(threads))
+    if rc != 0:
+        raise ValueError("oracle_dpd: bad schedule or period")
+    return out
+
+
+def motion_mt(frames: np.ndarray, w: int, h: int, fmt: int = 3, threshold: int = 32, prev_rgb=None,
+              threads: int | None = None) -> np.ndarray:
+    """motion_rgb (fmt 3) / motion_gray (fmt 1) over frame ranges in parallel; bit-identical."""
+    frames = np.ascontiguousarray(frames, np.uint8).reshape(-1)
+    count = frames.size // (fmt * w * h)
+    out = np.empty(count * w * h, np.uint8)
+    prev = None if prev_rgb is None else np.ascontiguousarray(prev_rgb, np.uint8).reshape(-1)
+    port().orc_motion_mt(_ptr(frames), count, w, h, fmt, threshold, None if prev is None else _ptr(prev), _ptr(out),
+                         _threads(threads))
     return out
 
 

@@ -58,13 +58,36 @@ def exchange_tail(send_tail, recv_buf, rank: int, world: int):
     return rank > 0
 
 
-class PeerBuffer:
-    """Rank r's view of rank r-1's exported shard buffer (CUDA IPC): set up
-    once (handles travel by all_gather_object -- setup, not the data path);
-    halos are then pulled with copy-engine peer copies over NVLink
-    (df_halo_copy), off the compute stream."""
+def dpd_halo_tails(schedule, ranges, period: int, taps: int, rank: int, peers: dict) -> list:
+    """Per branch, a device pointer to the last T-1 raw samples of its last
+    active block before this rank's block range -- wherever that block is:
+    on the previous rank, or on any earlier one when the branch is gated off
+    for whole shards (the frozen history of dpd.cpp:264-279) --
+    or None (zero history).  ranges: every rank's [start, end) sample range;
+    peers: rank -> base pointer of that rank's mapped shard (PeerBuffer)."""
+    b0 = ranges[rank][0] // period
+    out = []
+    for b in range(1, 11):
+        hb = dpd_halo_block(schedule, b0, b)
+        if hb is None:
+            out.append(None)
+            continue
+        owner = next(r for r, (s0, s1) in enumerate(ranges) if s0 // period <= hb < s1 // period)
+        local = hb - ranges[owner][0] // period
+        out.append(peers[owner] + 8 * ((local + 1) * period - (taps - 1)))
+    return out
 
-    def __init__(self, ptr: int, device: int, rank: int, world: int):
+
+class PeerBuffer:
+    """Rank r's views of the lower ranks' exported shard buffers (CUDA IPC):
+    set up once (handles travel by all_gather_object -- setup, not the data
+    path).  `ptr` / `device` are rank r-1's (the motion halo); `peers` maps
+    every lower rank to its mapped base pointer (a DPD branch gated off for
+    whole shards takes its FIR-history halo from further back).  Halos are
+    pulled with copy-engine peer copies over NVLink (df_halo_copy) or read by
+    the firing itself (df_dpd_fire_halo)."""
+
+    def __init__(self, ptr: int, device: int, rank: int, world: int, lower: str = "all"):
         import ctypes as C
 
         import torch.distributed as dist
@@ -78,15 +101,23 @@ class PeerBuffer:
         dist.all_gather_object(every, mine)
         self.ptr = None
         self.device = None
-        if rank > 0:
-            handle, self.device = every[rank - 1]
+        self.peers: dict[int, int] = {}
+        self._mapped: list[int] = []
+        wanted = range(rank) if lower == "all" else ([rank - 1] if rank > 0 else [])
+        for r in wanted:
+            handle, dev = every[r]
             hb = (C.c_char * n).from_buffer_copy(handle)
             p = C.c_void_p()
             _lib.call("df_ipc_open_handle", device, hb, C.byref(p))
-            self.ptr = p.value
+            self.peers[r] = p.value
+            self._mapped.append(p.value)
+            if r == rank - 1:
+                self.ptr, self.device = p.value, dev
 
     def close(self):
-        if self.ptr:
-            from . import _lib
-            _lib.call("df_ipc_close_handle", __import__("ctypes").c_void_p(self.ptr))
-            self.ptr = None
+        from . import _lib
+        for p in self._mapped:
+            _lib.call("df_ipc_close_handle", __import__("ctypes").c_void_p(p))
+        self._mapped = []
+        self.peers = {}
+        self.ptr = None

@@ -1,15 +1,19 @@
-"""GPU, BASELINE full sizes (the bench's own configs): the oracle is too slow
-for whole streams, so parity at full size is shown by size-independent
-properties plus oracle checks of sampled frames / blocks (each computed
-from exactly the inputs it depends on):
+"""GPU, BASELINE full sizes (the bench's own configs), WHOLE-output parity:
+every byte / float word of the GPU output against the oracle on the same
+stream.  The oracle runs in parallel over frame / block ranges
+(oracle.motion_mt / dpd_mt: each range starts from exactly the state the
+serial run has there -- the previous frame's gauss, each branch's FIR
+history from its active stream -- and tests/test_oracle.py pins them
+bit-identical to the serial restatement).
 
-* motion 1280x720 RGB x 300 and 3840x2160 RGB x 40: one firing == the same
-  frames in uneven firings (delay token carried; different M3 plans), and
-  sampled masks == the oracle on (frame f-2 as halo, f-1, f);
-* DPD-5 (10 branches x 32 taps, 2^27 samples) and DPD-3 (ramp, 4096-sample
-  blocks, 2^26): one batch == two batches (FirState carried), the leading
-  2^20 samples and sampled blocks == the oracle on the blocks they depend
-  on (history reaches back at most one block for DPD-5, 10 for the ramp).
+* motion 1280x720 RGB x 300 (configs[1]) and 3840x2160 RGB x 40 per GPU
+  (configs[3]): byte-exact, in one firing and in uneven firings (delay
+  token carried across firings; different M3 plans);
+* DPD-1 exactly as benched (first_n(2), 2^20, period 65536, configs[0]),
+  DPD-3 (ramp 1->10 branches, 4096-sample blocks, 2^26, configs[2]) and
+  DPD-5 (10 branches x 32 taps, 2^27 per GPU, configs[4]): bit-exact, in one
+  batch and in two (FirState and schedule position carried).
+Reference comparators: proj/src/bench.cpp:288-326.
 """
 import numpy as np
 import pytest
@@ -33,19 +37,13 @@ def _motion_host(rgb, w, h, splits):
 
 @pytest.mark.parametrize("w,h,n,splits", [(1280, 720, 300, (97, 103, 100)), (3840, 2160, 40, (13, 27))])
 def test_motion_full_size(gpu, w, h, n, splits):
-    fb, px = w * h * 3, w * h
-    rgb = O.synth_bytes(n * fb, 20240 + w)
+    rgb = O.synth_bytes(n * w * h * 3, 20240 + w)
+    want = O.motion_mt(rgb, w, h, 3, 32)
     whole = _motion_host(rgb, w, h, (n,))
-    assert np.array_equal(whole, _motion_host(rgb, w, h, splits)), "firing split changed the masks"
-    for f in (0, 1, splits[0], n // 2 + 1, n - 1):
-        if f == 0:
-            want = O.motion_rgb(rgb[:fb], w, h, 32)
-        elif f == 1:
-            want = O.motion_rgb(rgb[:2 * fb], w, h, 32)[px:]
-        else:
-            want = O.motion_rgb(rgb[(f - 1) * fb:(f + 1) * fb], w, h, 32, rgb[(f - 2) * fb:(f - 1) * fb])[px:]
-        got = whole[f * px:(f + 1) * px]
-        assert np.array_equal(got, want), f"frame {f}: {(got != want).sum()} bytes differ"
+    bad = np.nonzero(whole != want)[0]
+    assert bad.size == 0, f"{bad.size} bytes differ, first in frame {bad[0] // (w * h)}"
+    split = _motion_host(rgb, w, h, splits)
+    assert np.array_equal(split, want), "uneven firings changed the masks"
 
 
 def _dpd_host(x, taps, sched, period, splits):
@@ -67,26 +65,25 @@ def _bits(a):
     return np.ascontiguousarray(a).view(np.uint32)
 
 
-@pytest.mark.parametrize("name", ["dpd5", "dpd3"])
+@pytest.mark.parametrize("name", ["dpd1", "dpd3", "dpd5"])
 def test_dpd_full_size(gpu, name):
-    if name == "dpd5":
-        samples, period, T = 1 << 27, 65536, 32
-        sched = np.array([0x3FF], np.uint16)
-        back = 1
-    else:
+    if name == "dpd1":  # bench.py dpd1: first_n(2)
+        samples, period, T = 1 << 20, 65536, 10
+        sched = np.array([0x003], np.uint16)
+    elif name == "dpd3":  # ramp: block i -> first_n(1 + i % 10)
         samples, period, T = 1 << 26, 4096, 10
         sched = np.array([(1 << (1 + i % 10)) - 1 for i in range(10)], np.uint16)
-        back = 10
+    else:  # all ten branches, 32 taps
+        samples, period, T = 1 << 27, 65536, 32
+        sched = np.array([0x3FF], np.uint16)
     blocks = samples // period
     x = O.synth_samples(samples, 8080 + T)
     taps = O.random_taps(8081, T)
+    want = O.dpd_mt(x, taps, sched, period)
     whole = _dpd_host(x, taps, sched, period, (blocks,))
+    bad = np.nonzero(_bits(whole) != _bits(want))[0]
+    assert bad.size == 0, f"{bad.size} float words differ, first at sample {bad[0] // 2}"
+    idx, worst = O.compare_samples(whole, want)
+    assert idx < 0, worst
     split = _dpd_host(x, taps, sched, period, (blocks // 3, blocks - blocks // 3))
-    assert np.array_equal(_bits(whole), _bits(split)), "batch split changed the output"
-    lead = 1 << 20
-    assert np.array_equal(_bits(whole[:2 * lead]), _bits(O.dpd(x[:2 * lead], taps, sched, period)))
-    for k in (blocks // 3, blocks // 2 + 7, blocks - 1):
-        k0 = k - back
-        seg = O.dpd(x[2 * k0 * period:2 * (k + 1) * period], taps, np.roll(sched, -(k0 % len(sched))), period)
-        got = whole[2 * k * period:2 * (k + 1) * period]
-        assert np.array_equal(_bits(got), _bits(seg[2 * back * period:])), f"block {k} differs"
+    assert np.array_equal(_bits(split), _bits(want)), "batch split changed the output"

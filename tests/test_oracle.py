@@ -145,3 +145,29 @@ def test_oracle_vs_compiled_reference_motion_sizes():
         want = np.empty_like(f)
         R.ref_oracle_motion(P(f), n, w, h, thr, P(want))
         np.testing.assert_array_equal(O.motion_gray(f, w, h, thr), want)
+
+
+@pytest.mark.parametrize("period,T,blocks", [(64, 10, 37), (4, 10, 50), (7, 32, 40), (256, 32, 12), (1, 10, 60)])
+def test_dpd_mt_equals_serial(period, T, blocks):
+    """The threaded oracle (block ranges, FIR history rebuilt from each
+    branch's active stream) is bit-identical to the serial restatement,
+    including blocks shorter than T-1 and branches gated off for long runs."""
+    x = O.synth_samples(period * blocks, 5 + T)
+    taps = O.random_taps(6, T)
+    sched = np.array([0x3FF, 0x001, 0x200, 0x000, 0x2A5, 0x100, 0x100, 0x0F0, 0x001, 0x155, 0x300], np.uint16)
+    want = O.dpd(x, taps, sched, period)
+    for threads in (1, 3, 7):
+        np.testing.assert_array_equal(O.dpd_mt(x, taps, sched, period, threads).view(np.uint32), want.view(np.uint32))
+
+
+@pytest.mark.parametrize("fmt", [1, 3])
+def test_motion_mt_equals_serial(fmt):
+    w, h, n = 40, 24, 23
+    f = O.synth_bytes(n * w * h * fmt, 77)
+    want = O.motion_rgb(f, w, h, 32) if fmt == 3 else O.motion_gray(f, w, h, 32)
+    for threads in (1, 4, 9):
+        np.testing.assert_array_equal(O.motion_mt(f, w, h, fmt, 32, threads=threads), want)
+    if fmt == 3:
+        halo = O.synth_bytes(w * h * 3, 78)
+        np.testing.assert_array_equal(O.motion_mt(f, w, h, 3, 32, prev_rgb=halo, threads=5),
+                                      O.motion_rgb(f, w, h, 32, halo))
