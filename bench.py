@@ -552,29 +552,43 @@ def bench_dpd_ours(args, p, rank, world, local):
 
 
 # ------------------------------------------------------------------ CPU
-def cpu_motion(p, steps, warmup, threads=None, frames_per_net=None):
-    """Reference dynflow motion network (5 actor threads each) on gray(RGB)
-    (on the gray frames directly for a gray workload), several independent
-    networks on disjoint frame ranges to use the host cores; falls back to
-    the single-thread oracle port."""
+def cpu_motion(p, steps, warmup, nets=None):
+    """The reference's own dynflow motion network (5 actor threads,
+    proj/src/motion.cpp:107-218) on the FULL configuration: one step is all
+    of the workload's frames (300 at 720p), split into `nets` contiguous
+    frame ranges run as concurrent networks to use the host's cores (the
+    frame-range sharding our multi-GPU path uses).  value = the reference's
+    own metric, frames / active_seconds("sink") (proj/src/bench.cpp:
+    341-347), with the sink-active window of concurrent networks taken as
+    the longest one; median over steps.  Wall time per step (network build,
+    thread spawn, fill and drain included) is reported beside it.  RGB input
+    is converted to gray before the run (the reference takes gray frames).
+    Falls back to the single-thread oracle port without oracle/_ref."""
     from oracle import oracle as O
-    W, H = p["w"], p["h"]
+    W, H, F = p["w"], p["h"], p["frames"]
     rgb_in = p.get("fmt", 3) == 3
-    ncpu = os.cpu_count() or 1
+    ncpu = len(os.sched_getaffinity(0))
     if O.ref_available():
         R = O.ref()
-        nets = threads or max(1, ncpu // 5)
-        fpn = frames_per_net or 8
-        frames_in = O.synth_bytes(fpn * W * H * (3 if rgb_in else 1), 5)
-        outs = [np.empty(fpn * W * H, np.uint8) for _ in range(nets)]
+        # 8 networks on the 16-core box: gauss and med are the two busy actor
+        # threads of a network (3 / 5 / 8 networks: 177 / 281 / 392 frames/s,
+        # profiles/r02_cpu_baseline_probe.txt).
+        nets = nets or int(os.environ.get("DF_CPU_NETS", "0")) or max(1, ncpu // 2)
+        frames_in = O.synth_bytes(F * W * H * (3 if rgb_in else 1), 5)
+        gray = O.rgb_to_gray(frames_in) if rgb_in else frames_in
+        ranges = [(F * i // nets, F * (i + 1) // nets) for i in range(nets)]
+        out = np.empty(F * W * H, np.uint8)
+        act = [0.0] * nets
 
         def one(i):
-            gray = O.rgb_to_gray(frames_in) if rgb_in else frames_in
+            f0, f1 = ranges[i]
             a, w_ = C.c_double(), C.c_double()
-            R.ref_motion_network(gray.ctypes.data_as(C.c_void_p), fpn, W, H, 32, 1,
-                                 outs[i].ctypes.data_as(C.c_void_p), C.byref(a), C.byref(w_))
+            rc = R.ref_motion_network(gray[f0 * W * H:].ctypes.data_as(C.c_void_p), f1 - f0, W, H, 32, 1,
+                                      out[f0 * W * H:].ctypes.data_as(C.c_void_p), C.byref(a), C.byref(w_))
+            assert rc == 0
+            act[i] = a.value
 
-        times = []
+        active, wall = [], []
         for s in range(warmup + steps):
             ts = [threading.Thread(target=one, args=(i,)) for i in range(nets)]
             a = time.perf_counter()
@@ -583,19 +597,23 @@ def cpu_motion(p, steps, warmup, threads=None, frames_per_net=None):
             for t in ts:
                 t.join()
             if s >= warmup:
-                times.append(time.perf_counter() - a)
-        t = statistics.median(times)
-        return {"value": round(nets * fpn / t, 2), "unit": "frames/s", "cores": min(ncpu, 5 * nets),
-                "kind": "reference",
-                "sample": f"{nets} concurrent dynflow motion networks (5 actor threads each) x {fpn} frames "
-                          f"{W}x{H}" + (", gray(RGB) conversion included" if rgb_in else " gray")
-                          + f"; median of {steps}"}
-    frames_in = O.synth_bytes(4 * W * H * (3 if rgb_in else 1), 5)
+                wall.append(time.perf_counter() - a)
+                active.append(max(act))
+        return {"value": round(F / statistics.median(active), 2), "unit": "frames/s",
+                "cores": min(ncpu, 5 * nets), "kind": "reference",
+                "wall_value": round(F / statistics.median(wall), 2),
+                "sample": f"full config: {F} frames {W}x{H} per step as {nets} concurrent dynflow motion networks "
+                          f"(5 actor threads each) on contiguous frame ranges"
+                          + (", gray(RGB) conversion outside the timed runs" if rgb_in else " (gray)")
+                          + f"; value = frames / sink-active seconds (bench.cpp:341-347, longest of the {nets}), "
+                            f"wall_value = frames / step wall time; median of {steps}"}
+    n = 4
+    frames_in = O.synth_bytes(n * W * H * (3 if rgb_in else 1), 5)
     a = time.perf_counter()
     (O.motion_rgb if rgb_in else O.motion_gray)(frames_in, W, H)
     t = time.perf_counter() - a
-    return {"value": round(4 / t, 2), "unit": "frames/s", "cores": 1, "kind": "port",
-            "sample": f"oracle port, 4 frames {W}x{H} {'RGB' if rgb_in else 'gray'}, 1 thread"}
+    return {"value": round(n / t, 2), "unit": "frames/s", "cores": 1, "kind": "port",
+            "sample": f"oracle port, {n} frames {W}x{H} {'RGB' if rgb_in else 'gray'}, 1 thread"}
 
 
 def cpu_dpd(p, steps, warmup):
@@ -616,7 +634,7 @@ def cpu_dpd(p, steps, warmup):
     sched = dpd_schedule(p["sched"], n // period)
     x = O.synth_samples(n, 810)
     taps = O.random_taps(808, T)
-    ncpu = os.cpu_count() or 1
+    ncpu = len(os.sched_getaffinity(0))
     use_ref = O.ref_available() and T == 10 and all(bin(int(m)).count("1") >= 2 for m in sched)
     use_ref_oracle = O.ref_available() and T == 10 and not use_ref
     sc = np.ascontiguousarray(sched)
@@ -632,8 +650,9 @@ def cpu_dpd(p, steps, warmup):
         else:
             O.dpd(x, taps, sched, period)
 
-    times = []
-    for s in range(warmup + steps):
+    times, walls = [], []
+    reps = max(steps, 5) if use_ref else steps  # cmd_dpd: median of 5 reps (bench.cpp:391-397)
+    for s in range(warmup + reps):
         if use_ref:
             R = O.ref()
             a_, w_ = C.c_double(), C.c_double()
@@ -641,8 +660,10 @@ def cpu_dpd(p, steps, warmup):
             rc = R.ref_dpd_network(x.ctypes.data_as(C.c_void_p), n, taps.ctypes.data_as(C.c_void_p),
                                    sc.ctypes.data_as(C.c_void_p), sc.size, period, outs[0].ctypes.data_as(C.c_void_p),
                                    C.byref(a_), C.byref(w_))
-            el = time.perf_counter() - a
             assert rc == 0
+            if s >= warmup:
+                walls.append(time.perf_counter() - a)
+            el = a_.value  # the reference's metric: samples / active_seconds("sink")
         else:
             ts = [threading.Thread(target=one, args=(i,)) for i in range(workers)]
             a = time.perf_counter()
@@ -655,8 +676,12 @@ def cpu_dpd(p, steps, warmup):
             times.append(el)
     t = statistics.median(times)
     if use_ref:
+        full = n == p["samples"]
         return {"value": round(n / t / 1e6, 2), "unit": "Msamples/s", "cores": min(ncpu, 15), "kind": "reference",
-                "sample": f"dynflow DPD network (15 actor threads), {n} samples, period {period}; median of {steps}"}
+                "wall_value": round(n / statistics.median(walls) / 1e6, 2),
+                "sample": f"{'full config: ' if full else ''}dynflow DPD network (15 actor threads), {n} samples, "
+                          f"period {period}; value = samples / sink-active seconds (cmd_dpd, bench.cpp:391-397), "
+                          f"wall_value = samples / run() wall time; median of {reps}"}
     if use_ref_oracle:
         return {"value": round(workers * n / t / 1e6, 2), "unit": "Msamples/s", "cores": workers,
                 "kind": "reference",
@@ -761,6 +786,30 @@ def dpd_network(p, steps, warmup):
                     "-> out channel -> sink; host-endpoint commits are 1-thread kernels"}
 
 
+def resident_networks():
+    """The reference's own network shapes (15-actor DPD, 5-actor motion with
+    its delay channel) as device-resident actors -- one persistent kernel,
+    control tokens dispatched per firing on the device (dfh_*_run_resident)
+    -- measured by the reference's metric (units / active_seconds("sink")).
+    DPD-1's full configuration; motion 1280x720 x 300 in the reference's
+    gray format (that network has no RGB front end)."""
+    from oracle import oracle as O
+    from paper_1611_03226_b200 import host_api as H
+    x = O.synth_samples(1 << 20, 810)
+    taps = O.random_taps(808)
+    H.dpd_run_resident(x, taps, [3], 65536)
+    ms = [H.dpd_run_resident(x, taps, [3], 65536)[1] for _ in range(3)]
+    f = O.synth_bytes(300 * 1280 * 720, 5)
+    mm = [H.motion_run_resident(f, 1280, 720, 32)[1] for _ in range(2)]
+    return {"dpd1": {"value": round((1 << 20) / (statistics.median(ms) / 1e3) / 1e6, 1), "unit": "Msamples/s",
+                     "path": "dfh_dpd_run_resident: source, config, split, 10 branches, adder, sink (56 channels), "
+                             "16 CTAs per branch"},
+            "motion720gray": {"value": round(300 / (statistics.median(mm) / 1e3), 1), "unit": "frames/s",
+                              "path": "dfh_motion_run_resident: source, gauss, thres, med, sink with the "
+                                      "gauss_thres_prev delay channel, 64 CTAs per actor"},
+            "metric": "units / sink-active seconds (bench.cpp:341-347, :391-397), device timestamps"}
+
+
 def bench_reference(args, kind, p, rank, world):
     if rank != 0:
         return None
@@ -830,6 +879,7 @@ def main():
                              "cpu_baseline": cb}
                 if name == "dpd3":
                     sec[name]["network"] = dpd_network(WORKLOADS[name][1], 5, 3)
+            sec["resident_networks"] = resident_networks()
             res["secondary"] = sec
         print(json.dumps(res), flush=True)
     if world > 1:

@@ -65,6 +65,6 @@ inline constexpr unsigned kMaxHistory = 31;  // FirState samples for up to 32 ta
 // params.batch is ignored (one block per firing, as the reference).  Needs
 // source_firing_limit = samples / period.  branch_ctas: CTAs per branch
 // actor (source, split, adder and sink get half).
-NetworkGraph build_reference_network(const Params& params, int device = 0, std::uint32_t branch_ctas = 8);
+NetworkGraph build_reference_network(const Params& params, int device = 0, std::uint32_t branch_ctas = 16);
 
 }  // namespace df::dpd

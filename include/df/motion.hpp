@@ -35,7 +35,7 @@ std::uint64_t source_firings(const Params& params);
 // rate r on every channel) as DEVICE-RESIDENT actors, each run by `ctas`
 // CTAs of one persistent kernel.  Gray input only (the reference's format);
 // host spans staged to HBM by the source's init / back by the sink's finish.
-NetworkGraph build_reference_network(const Params& params, int device = 0, std::uint32_t ctas = 16);
+NetworkGraph build_reference_network(const Params& params, int device = 0, std::uint32_t ctas = 64);
 
 // Heterogeneous network (CPU + GPU actors on shared device channels, the
 // paper's mixed mapping): source (H2D, RGB) -> gray (CPU actor: BT.601

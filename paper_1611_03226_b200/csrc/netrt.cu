@@ -116,46 +116,53 @@ __device__ void raise_fault(NetCtl* ctl, int actor, unsigned code, unsigned toke
   atomicExch(&ctl->abort, 1u);
 }
 
-// Is the run aborted (a device fault, or df_net_abort from the host)?  A
-// host abort is promoted to the device word so every actor sees it.
-__device__ bool aborted_now(NetCtl* ctl) {
-  if (*(volatile unsigned*)&ctl->abort) return true;
-  if (*ctl->host_abort) {
-    atomicCAS(&ctl->fault_code, 0u, (unsigned)DF_EABORTED);
-    atomicExch(&ctl->abort, 1u);
-    return true;
-  }
-  return false;
+// Polls the mapped host abort word (df_net_abort) -- a PCIe read, so only
+// group leaders poll it, at most every kHostPollNs -- and promotes it to the
+// device word every actor watches.
+constexpr unsigned long long kHostPollNs = 20000;
+__device__ bool host_abort_poll(NetCtl* ctl, unsigned long long* last) {
+  const unsigned long long t = now_ns();
+  if (t - *last < kHostPollNs) return false;
+  *last = t;
+  if (!*ctl->host_abort) return false;
+  atomicCAS(&ctl->fault_code, 0u, (unsigned)DF_EABORTED);
+  atomicExch(&ctl->abort, 1u);
+  return true;
 }
 
+// Is the run aborted (a device fault, or df_net_abort from the host)?
+__device__ bool aborted_now(NetCtl* ctl, unsigned long long* last_host_poll) {
+  if (*(volatile unsigned*)&ctl->abort) return true;
+  return last_host_poll && host_abort_poll(ctl, last_host_poll);
+}
+
+// A wait loop: backs off from 32 ns to ~1 us between polls, watches the
+// abort words, and (leaders) a watchdog over the whole wait.
 struct Spin {
   unsigned long long t0 = 0;
+  unsigned long long* host_poll = nullptr;  // leaders: their last host-abort poll time
   unsigned n = 0;
-  bool watchdog = true;  // false: only the abort words end the wait
+  bool watchdog = true;
   // Returns kAbort when the run is aborted or this wait timed out.
   __device__ int tick(NetCtl* ctl, int actor) {
-    if (*(volatile unsigned*)&ctl->abort) return kAbort;
-    if ((++n & 63) == 0) {
-      if (*ctl->host_abort) {
-        atomicCAS(&ctl->fault_code, 0u, (unsigned)DF_EABORTED);
-        atomicExch(&ctl->abort, 1u);
-        return kAbort;
-      }
+    if (aborted_now(ctl, (++n & 15) == 0 ? host_poll : nullptr)) return kAbort;
+    if (watchdog && (n & 15) == 0) {
       const unsigned long long t = now_ns();
       if (t0 == 0) t0 = t;
-      if (watchdog && t - t0 > ctl->timeout_ns) {
+      if (t - t0 > ctl->timeout_ns) {
         raise_fault(ctl, actor, DF_ETIMEOUT, 0);
         return kAbort;
       }
     }
-    __nanosleep(n < 64 ? 32 : 256);
+    __nanosleep(32u << min(n / 8, 5u));
     return kOk;
   }
 };
 
 // read_start (channel.cpp:114-140): r tokens, or end of stream once closed.
-__device__ int wait_readable(const DevChan& c, unsigned r, NetCtl* ctl, int actor) {
+__device__ int wait_readable(const DevChan& c, unsigned r, NetCtl* ctl, int actor, unsigned long long* poll) {
   Spin s;
+  s.host_poll = poll;
   for (;;) {
     if (ld_acq64(&c.st->available) >= r) return kOk;
     if (ld_acq32(&c.st->closed)) return ld_acq64(&c.st->available) >= r ? kOk : kEos;
@@ -163,8 +170,9 @@ __device__ int wait_readable(const DevChan& c, unsigned r, NetCtl* ctl, int acto
   }
 }
 // write_start (channel.cpp:63-89): room for r tokens (distinct capacity).
-__device__ int wait_writable(const DevChan& c, unsigned r, NetCtl* ctl, int actor) {
+__device__ int wait_writable(const DevChan& c, unsigned r, NetCtl* ctl, int actor, unsigned long long* poll) {
   Spin s;
+  s.host_poll = poll;
   const unsigned long long cap = chan_distinct_capacity(c.rate, c.has_delay);
   for (;;) {
     if (ld_acq64(&c.st->available) + r <= cap) return kOk;
@@ -209,12 +217,13 @@ __device__ __forceinline__ const P& params(const ActorDesc& A) {
 
 // ---- leader: one firing's control, regions and waits ----------------------
 // Fills rt->frame and publishes it (returns false once the actor stops).
-__device__ bool leader_prepare(const ActorDesc& A, int a, ActorRt* rt, NetCtl* ctl, bool* aborted) {
+__device__ bool leader_prepare(const ActorDesc& A, int a, ActorRt* rt, NetCtl* ctl, bool* aborted,
+                               unsigned long long* poll) {
   Frame& F = rt->frame;
   const unsigned long long i = rt->firings;
   bool stop = false;
   if (A.limit && i >= A.limit) stop = true;  // source firing limit (runtime.cpp:217-219)
-  if (!stop && aborted_now(ctl)) {  // checked once per firing, not only inside waits
+  if (!stop && aborted_now(ctl, poll)) {  // checked once per firing, not only inside waits
     stop = true;
     *aborted = true;
   }
@@ -226,7 +235,7 @@ __device__ bool leader_prepare(const ActorDesc& A, int a, ActorRt* rt, NetCtl* c
     if (P.stall_mask && (mix64(P.seed ^ (i * 0x51ed27ull)) & P.stall_mask) == 0) pause += 2000;
     const unsigned long long t0 = now_ns();
     while (pause && now_ns() - t0 < pause) {
-      if (aborted_now(ctl)) {
+      if (aborted_now(ctl, poll)) {
         stop = true;
         *aborted = true;
         break;
@@ -235,7 +244,7 @@ __device__ bool leader_prepare(const ActorDesc& A, int a, ActorRt* rt, NetCtl* c
     }
   }
   if (!stop && A.has_ctrl) {  // fire_once: one control token, then rates
-    const int w = wait_readable(A.ctrl, 1, ctl, a);
+    const int w = wait_readable(A.ctrl, 1, ctl, a, poll);
     if (w != kOk) {
       stop = true;
       *aborted = w == kAbort;
@@ -259,7 +268,7 @@ __device__ bool leader_prepare(const ActorDesc& A, int a, ActorRt* rt, NetCtl* c
   }
   for (unsigned p = 0; !stop && p < A.n_in; ++p) {
     if (!((in_on >> p) & 1u)) continue;
-    const int w = wait_readable(A.in[p], A.in[p].rate, ctl, a);
+    const int w = wait_readable(A.in[p], A.in[p].rate, ctl, a, poll);
     if (w != kOk) {
       stop = true;
       *aborted = w == kAbort;
@@ -270,7 +279,7 @@ __device__ bool leader_prepare(const ActorDesc& A, int a, ActorRt* rt, NetCtl* c
   unsigned wrap = 0;
   for (unsigned p = 0; !stop && p < A.n_out; ++p) {
     if (!((out_on >> p) & 1u)) continue;
-    const int w = wait_writable(A.out[p], A.out[p].rate, ctl, a);
+    const int w = wait_writable(A.out[p], A.out[p].rate, ctl, a, poll);
     if (w != kOk) {
       stop = true;
       *aborted = true;
@@ -556,12 +565,13 @@ __device__ void post_kind(const ActorDesc& A, const Frame& F, ActorRt* rt) {
 
 // Leader, after the loop: close outputs, then drain inputs until their
 // producers close (runtime.cpp:223-229, drain_channel :199-204).
-__device__ void leader_finish(const ActorDesc& A, int a, ActorRt* rt, NetCtl* ctl, bool aborted) {
+__device__ void leader_finish(const ActorDesc& A, int a, ActorRt* rt, NetCtl* ctl, bool aborted,
+                              unsigned long long* poll) {
   rt->t_stop = now_ns();
   for (unsigned p = 0; p < A.n_out; ++p) close_channel(A.out[p]);
   if (aborted) return;
   auto drain = [&](const DevChan& c) {
-    while (wait_readable(c, c.rate, ctl, a) == kOk) commit_read(c, c.rate);
+    while (wait_readable(c, c.rate, ctl, a, poll) == kOk) commit_read(c, c.rate);
   };
   for (unsigned p = 0; p < A.n_in; ++p) drain(A.in[p]);
   if (A.has_ctrl) drain(A.ctrl);
@@ -587,11 +597,12 @@ __global__ void __launch_bounds__(kNetThreads) net_kernel(const ActorDesc* __res
   const Group G{blockIdx.x - A.cta0, A.ctas};
   const bool leader_cta = G.g == 0;
   unsigned gen = 0;
+  unsigned long long host_poll = 0;  // leader thread: last poll of the host abort word
   for (;;) {
     if (threadIdx.x == 0) {
       if (leader_cta) {
         bool ab = false;
-        leader_prepare(A, a, rt, ctl, &ab);
+        leader_prepare(A, a, rt, ctl, &ab, &host_poll);
         s_aborted = ab;
       } else {
         Spin s;
@@ -653,7 +664,8 @@ __global__ void __launch_bounds__(kNetThreads) net_kernel(const ActorDesc* __res
       ++rt->firings;
     }
   }
-  if (leader_cta && threadIdx.x == 0) leader_finish(A, a, rt, ctl, s_aborted || *(volatile unsigned*)&ctl->abort);
+  if (leader_cta && threadIdx.x == 0)
+    leader_finish(A, a, rt, ctl, s_aborted || *(volatile unsigned*)&ctl->abort, &host_poll);
 }
 
 }  // namespace

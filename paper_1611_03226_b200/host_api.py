@@ -123,7 +123,7 @@ MOTION_ACTORS = ["source", "gauss", "thres", "med", "sink"]
 
 
 def dpd_run_resident(inp: np.ndarray, taps: np.ndarray, schedule, period: int, device: int = 0,
-                     allow_single_branch: bool = False, branch_ctas: int = 8, timeout_s: float = 30.0):
+                     allow_single_branch: bool = False, branch_ctas: int = 16, timeout_s: float = 30.0):
     """The reference's 15-actor DPD network as device-resident actors (one
     persistent kernel); returns (output, sink_active_ms, {actor: firings},
     channel tokens written [56])."""
@@ -144,7 +144,7 @@ def dpd_run_resident(inp: np.ndarray, taps: np.ndarray, schedule, period: int, d
 
 
 def motion_run_resident(frames: np.ndarray, width: int, height: int, threshold: int = 32, rate: int = 1,
-                        device: int = 0, ctas: int = 16, timeout_s: float = 30.0):
+                        device: int = 0, ctas: int = 64, timeout_s: float = 30.0):
     """The reference's 5-actor motion network (gauss_thres_prev delay channel)
     as device-resident actors; returns (masks, sink_active_ms, {actor: firings})."""
     frames = np.ascontiguousarray(frames, np.uint8).reshape(-1)
