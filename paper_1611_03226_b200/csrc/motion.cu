@@ -80,6 +80,7 @@ struct MotionGeom {
   // its weights straight from the constant bank (no per-step UMOVs).
   unsigned wg[6];    // gray
   unsigned wh[8];    // horizontal gauss
+  int l2hint;        // M3: L2 eviction hints on band-halo rows (large frames)
 };
 
 
@@ -582,8 +583,8 @@ constexpr size_t kSmemBytes = sizeof(uint2) * kWarpsPerCta * (kBandRows + 2) * 3
 // this path has no MMA) and streams the input rows through a per-warp
 // shared-memory ring filled by TMA (cp.async.bulk.tensor, one box of kM3RPS
 // rows per issue, mbarrier completion), kM3Stages * kM3RPS rows ahead of the
-// consumer.  Out-of-frame rows/columns come back zero-filled (OOB) or as a
-// neighbouring frame's rows; both only reach border rows/columns, which the
+// consumer.  Out-of-frame rows and columns come back zero-filled (OOB: a 3-D
+// (column, row, frame) view); they only reach border rows/columns, which the
 // reference copies (motion.cpp:34-37, :64-67).
 //
 // CTA = kM3Warps warps on the same (tile, band), each walking its own frame
@@ -653,12 +654,48 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
         : "memory");
   } while (!done);
 }
-__device__ __forceinline__ void tma_load_2d(unsigned dst, const CUtensorMap* map, int c0, int c1, unsigned bar) {
+#ifndef DF_M3_TMA3D
+#define DF_M3_TMA3D 1
+#endif
+// 3-D tensor (column word, row, frame): rows outside [0, H) of a frame are
+// out of bounds and zero-filled without a DRAM read (a 2-D rows x frames
+// view would fetch the neighbouring frame's rows for the top and bottom
+// bands: 5.3 % extra input reads at 720p).
+__device__ __forceinline__ void tma_load_3d(unsigned dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            unsigned bar) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
       : "memory");
 }
+// Same load with an L2 eviction-priority policy (createpolicy).
+__device__ __forceinline__ void tma_load_3d_hint(unsigned dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                                 unsigned bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// L2 hints on the row stream (MotionGeom::l2hint; A/B in
+// profiles/r02_ab_motion_l2hint.txt).  The 6 rows a band shares with the
+// band above are read FIRST by this band (top of its pass) and LAST by the
+// band above (bottom of its pass), one frame pass later.  At 4K that pass
+// streams ~10x more bytes than at 720p and the rows are gone from L2 by the
+// second read; the hint loads the first two groups of a pass with
+// evict_last and the last group (the rows the band below already read) with
+// evict_first.  4K RGB: 0.267 -> 0.250 ms (0.76 -> 0.81 of HBM); 720p: 1 %
+// slower (its halo rows already survive), so it is enabled per geometry.
 __device__ __forceinline__ void tmem_st2(unsigned taddr, unsigned a, unsigned b) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(taddr), "r"(a), "r"(b) : "memory");
 }
@@ -684,6 +721,7 @@ struct M3Stream {
   const CUtensorMap* map;
   const CUtensorMap* hmap;  // inline halo: pass 0 reads frame 0 of this map
   bool hfirst;
+  bool l2hint;        // L2 eviction hints on the band-halo rows (MotionGeom::l2hint)
   unsigned ring;      // smem address of this warp's ring
   unsigned bars;      // smem address of this warp's kM3Stages mbarriers
   unsigned g;         // group being consumed
@@ -698,12 +736,22 @@ struct M3Stream {
   __device__ __forceinline__ void issue(unsigned gi, unsigned s) {  // lane 0 only
     if (gi >= groups) return;
     const unsigned pass = gi / GPP;
-    const int row = y0 - 3 + (int)(gi % GPP) * kM3RPS;
+    int row = y0 - 3 + (int)(gi % GPP) * kM3RPS;
     mbar_expect_tx(bars + 8 * s, kM3RPS * m3_row_bytes<FMT>());
-    if (hfirst && pass == 0)
-      tma_load_2d(ring + s * m3_stage_bytes<FMT>(), hmap, c0, row, bars + 8 * s);
+    const CUtensorMap* m = (hfirst && pass == 0) ? hmap : map;
+#if DF_M3_TMA3D
+    const int f = (hfirst && pass == 0) ? 0 : fs + (int)pass;
+#else  // A/B baseline: frames stacked on the row axis (frame f at row f*H)
+    const int f = 0;
+    row += (hfirst && pass == 0) ? 0 : (fs + (int)pass) * H;
+#endif
+    const unsigned in_pass = gi % GPP;
+    if (l2hint && in_pass < 2)
+      tma_load_3d_hint(ring + s * m3_stage_bytes<FMT>(), m, c0, row, f, bars + 8 * s, policy_evict_last());
+    else if (l2hint && in_pass == GPP - 1)
+      tma_load_3d_hint(ring + s * m3_stage_bytes<FMT>(), m, c0, row, f, bars + 8 * s, policy_evict_first());
     else
-      tma_load_2d(ring + s * m3_stage_bytes<FMT>(), map, c0, (fs + (int)pass) * H + row, bars + 8 * s);
+      tma_load_3d(ring + s * m3_stage_bytes<FMT>(), m, c0, row, f, bars + 8 * s);
   }
   __device__ __forceinline__ void acquire() {
     mbar_wait(bars + 8 * stage, phase);
@@ -949,6 +997,7 @@ __global__ void __launch_bounds__(32 * kM3Warps, DF_M3_MINB) motion_m3_kernel(co
   st.phase = 0;
   st.cur = 0;
   st.c0 = (tx0 * FMT - 8) / 4;  // 16-byte aligned box start (see m3_row_bytes)
+  st.l2hint = g.l2hint;
   st.H = g.H;
   st.y0 = y0;
   // Channel mode: the map covers the input channel's whole storage; the
@@ -1207,24 +1256,32 @@ int launch_m3(df_motion* m, const MotionIO& io, int frames, cudaStream_t s) {
     if (ri >= 0 && ri < 3) best = m3_plan(m, frames, ri);
   }
   g.chunk = best.chunk;
+  // Band-halo rows need the L2 hint only when a frame pass streams more than
+  // L2 can hold between their two reads (4K: 24.9 MB RGB frames; not 720p).
+  g.l2hint = (size_t)m->W * m->H * FMT >= (8u << 20) ? 1 : 0;
+  if (const char* force = getenv("DF_MOTION_L2HINT")) g.l2hint = atoi(force);
   // Raw mode: the map covers the firing's frames; channel mode: the input
   // channel's whole storage (the kernel offsets to its region).
   const void* base = io.channel_mode ? (const void*)io.in_ch.storage : (const void*)io.in;
   const unsigned long long map_frames =
       io.channel_mode ? chan_capacity_tokens(io.in_ch.rate, io.in_ch.has_delay) : (unsigned long long)frames;
   CUtensorMap map;
-  const cuuint64_t dims[2] = {(cuuint64_t)m->W * FMT / 4, (cuuint64_t)m->H * (cuuint64_t)map_frames};
-  const cuuint64_t strides[1] = {(cuuint64_t)m->W * FMT};
-  const cuuint32_t box[2] = {(cuuint32_t)(m3_row_bytes<FMT>() / 4), (cuuint32_t)kM3RPS};
-  const cuuint32_t estr[2] = {1, 1};
-  CUresult cr = tensor_map_encoder()(&map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void*>(base), dims,
+#if DF_M3_TMA3D
+  const cuuint64_t dims[3] = {(cuuint64_t)m->W * FMT / 4, (cuuint64_t)m->H, (cuuint64_t)map_frames};
+#else
+  const cuuint64_t dims[3] = {(cuuint64_t)m->W * FMT / 4, (cuuint64_t)m->H * map_frames, 1};
+#endif
+  const cuuint64_t strides[2] = {(cuuint64_t)m->W * FMT, (cuuint64_t)m->W * FMT * (cuuint64_t)m->H};
+  const cuuint32_t box[3] = {(cuuint32_t)(m3_row_bytes<FMT>() / 4), (cuuint32_t)kM3RPS, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult cr = tensor_map_encoder()(&map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<void*>(base), dims,
                                      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   DF_REQUIRE(cr == CUDA_SUCCESS, DF_ECUDA, "motion: cuTensorMapEncodeTiled failed (%d)", (int)cr);
   CUtensorMap hmap = map;
   if (io.halo) {  // one frame, same box
-    const cuuint64_t hdims[2] = {(cuuint64_t)m->W * FMT / 4, (cuuint64_t)m->H};
-    cr = tensor_map_encoder()(&hmap, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<unsigned char*>(io.halo), hdims,
+    const cuuint64_t hdims[3] = {(cuuint64_t)m->W * FMT / 4, (cuuint64_t)m->H, 1};
+    cr = tensor_map_encoder()(&hmap, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<unsigned char*>(io.halo), hdims,
                               strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     DF_REQUIRE(cr == CUDA_SUCCESS, DF_ECUDA, "motion: cuTensorMapEncodeTiled (halo) failed (%d)", (int)cr);
