@@ -371,6 +371,12 @@ int df_net_fault(const df_net* net, int* actor, int* code, uint32_t* token);
 /* After a run: firings, and device time from the first firing's start to
  * the actor's stop (RunStats::active_seconds, bench.cpp:346-347). */
 int df_net_actor_stats(const df_net* net, int actor, uint64_t* firings, double* active_ms);
+/* After a run, the actor leader's time split over all its firings (device
+ * timestamps): waiting for tokens / room (read_start + write_start and the
+ * control token), firing (frame published -> every CTA done), committing
+ * (phase-2 copies + counter updates).  Tracing aid (RunStats has no
+ * counterpart). */
+int df_net_actor_profile(const df_net* net, int actor, double* wait_ms, double* fire_ms, double* commit_ms);
 
 /* ---- multi-GPU halos (NVLink peer copies; no collectives) ---------------
  * No reference counterpart: dynflow is one CPU process.  These serve the

@@ -155,6 +155,7 @@ _SIGS = {
     "df_net_abort": (_i, [_vp]),
     "df_net_fault": (_i, [_vp, _P(_i), _P(_i), _P(_u32)]),
     "df_net_actor_stats": (_i, [_vp, _i, _P(_u64), _P(C.c_double)]),
+    "df_net_actor_profile": (_i, [_vp, _i, _P(C.c_double), _P(C.c_double), _P(C.c_double)]),
     "df_fill_random_u8": (_i, [_vp, _sz, _u64, _vp]),
     "df_fill_random_pm1": (_i, [_vp, _sz, _u64, _vp]),
     "df_kernel_launches": (_u64, []),

@@ -74,6 +74,10 @@ struct ActorRt {
   unsigned done;  // CTAs finished with the current frame
   Frame frame;
   unsigned long long firings, t_first, t_stop;
+  // Leader time split (ns, summed over firings): waiting in read_start /
+  // write_start (incl. the control token), firing (publish -> every CTA
+  // done), commit (phase-2 copies + counter updates).
+  unsigned long long t_wait, t_fire, t_commit;
   unsigned long long state[4];  // kind state (test stream positions)
 };
 
@@ -136,7 +140,7 @@ __device__ bool aborted_now(NetCtl* ctl, unsigned long long* last_host_poll) {
   return last_host_poll && host_abort_poll(ctl, last_host_poll);
 }
 
-// A wait loop: backs off from 32 ns to ~1 us between polls, watches the
+// A wait loop: backs off from 32 ns to 256 ns between polls, watches the
 // abort words, and (leaders) a watchdog over the whole wait.
 struct Spin {
   unsigned long long t0 = 0;
@@ -154,7 +158,7 @@ struct Spin {
         return kAbort;
       }
     }
-    __nanosleep(32u << min(n / 8, 5u));
+    __nanosleep(32u << min(n / 8, 3u));  // 32 ns .. 256 ns
     return kOk;
   }
 };
@@ -169,30 +173,39 @@ __device__ int wait_readable(const DevChan& c, unsigned r, NetCtl* ctl, int acto
     if (s.tick(ctl, actor) != kOk) return kAbort;
   }
 }
-// write_start (channel.cpp:63-89): room for r tokens (distinct capacity).
-__device__ int wait_writable(const DevChan& c, unsigned r, NetCtl* ctl, int actor, unsigned long long* poll) {
-  Spin s;
-  s.host_poll = poll;
-  const unsigned long long cap = chan_distinct_capacity(c.rate, c.has_delay);
-  for (;;) {
-    if (ld_acq64(&c.st->available) + r <= cap) return kOk;
-    if (s.tick(ctl, actor) != kOk) return kAbort;
-  }
-}
-// write_end / read_end: the group's data accesses are complete and fenced.
-__device__ void commit_write(const DevChan& c, unsigned r) {
+// write_end / read_end.  The CALLER fences once before a firing's commits
+// (every CTA's data accesses of the firing are complete by then); the
+// counter updates themselves are relaxed reductions.
+// `phase` is the endpoint's phase, cached by the leader (it is the only
+// writer); the control block's copy is written for the host's stats.
+__device__ void commit_write(const DevChan& c, unsigned r, unsigned& phase) {
   DevChanState* st = c.st;
-  st->write_phase = (st->write_phase + 1) % chan_phases(c.has_delay);
-  st->written += r;
-  __threadfence();
+  phase = (phase + 1) % chan_phases(c.has_delay);
+  st->write_phase = phase;
+  atomicAdd(&st->written, (unsigned long long)r);
   atomicAdd(&st->available, (unsigned long long)r);
 }
-__device__ void commit_read(const DevChan& c, unsigned r) {
+__device__ void commit_read(const DevChan& c, unsigned r, unsigned& phase) {
   DevChanState* st = c.st;
-  st->read_phase = (st->read_phase + 1) % chan_phases(c.has_delay);
-  st->read += r;
-  __threadfence();
+  phase = (phase + 1) % chan_phases(c.has_delay);
+  st->read_phase = phase;
+  atomicAdd(&st->read, (unsigned long long)r);
   atomicAdd(&st->available, (unsigned long long)(-(long long)r));
+}
+
+// The leader's cached endpoint phases (shared memory of the leader CTA).
+struct Phases {
+  unsigned in[kMaxPorts], out[kMaxPorts], ctrl;
+};
+__device__ __forceinline__ unsigned long long ld_rlx64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned ld_rlx32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
 __device__ void close_channel(const DevChan& c) {
   __threadfence();
@@ -218,7 +231,7 @@ __device__ __forceinline__ const P& params(const ActorDesc& A) {
 // ---- leader: one firing's control, regions and waits ----------------------
 // Fills rt->frame and publishes it (returns false once the actor stops).
 __device__ bool leader_prepare(const ActorDesc& A, int a, ActorRt* rt, NetCtl* ctl, bool* aborted,
-                               unsigned long long* poll) {
+                               unsigned long long* poll, Phases& ph) {
   Frame& F = rt->frame;
   const unsigned long long i = rt->firings;
   bool stop = false;
@@ -249,12 +262,13 @@ __device__ bool leader_prepare(const ActorDesc& A, int a, ActorRt* rt, NetCtl* c
       stop = true;
       *aborted = w == kAbort;
     } else {
-      const unsigned char* tok = A.ctrl.storage + chan_read_slot(A.ctrl.rate, A.ctrl.has_delay, A.ctrl.st->read_phase) * A.ctrl.token_size;
+      const unsigned char* tok = A.ctrl.storage + chan_read_slot(A.ctrl.rate, A.ctrl.has_delay, ph.ctrl) * A.ctrl.token_size;
       unsigned v = 0;
       for (unsigned b = 0; b < 4 && b < A.ctrl.token_size; ++b) v |= (unsigned)__ldcg(tok + b) << (8 * b);
       unsigned extra = 0;  // bytes beyond the 4th must be zero for v to name the token
       for (unsigned b = 4; b < A.ctrl.token_size && b < 64; ++b) extra |= __ldcg(tok + b);
-      commit_read(A.ctrl, 1);  // the control region is released before the firing (runtime.cpp:144)
+      __threadfence();  // the token bytes are read before the slot is released
+      commit_read(A.ctrl, 1, ph.ctrl);  // the control region is released before the firing (runtime.cpp:144)
       const uint32_t* row = A.table + 3ull * (v < A.domain ? v : 0);
       if (v >= A.domain || extra || !row[2]) {
         raise_fault(ctl, a, DF_ECONTROL, v);
@@ -266,28 +280,65 @@ __device__ bool leader_prepare(const ActorDesc& A, int a, ActorRt* rt, NetCtl* c
       }
     }
   }
-  for (unsigned p = 0; !stop && p < A.n_in; ++p) {
-    if (!((in_on >> p) & 1u)) continue;
-    const int w = wait_readable(A.in[p], A.in[p].rate, ctl, a, poll);
-    if (w != kOk) {
-      stop = true;
-      *aborted = w == kAbort;
-    } else {
-      F.in_ptr[p] = A.in[p].storage + chan_read_slot(A.in[p].rate, A.in[p].has_delay, A.in[p].st->read_phase) * A.in[p].token_size;
+  // read_start on every active input and write_start on every active
+  // output, polled together: each round issues all the counter loads
+  // (relaxed, independent) and spins only while some port is not ready; one
+  // acquire fence then orders the firing's data accesses after them.
+  if (!stop) {
+    unsigned in_wait = in_on & (A.n_in >= 32 ? 0xffffffffu : (1u << A.n_in) - 1);
+    unsigned out_wait = out_on & (A.n_out >= 32 ? 0xffffffffu : (1u << A.n_out) - 1);
+    Spin sp;
+    sp.host_poll = poll;
+    while (in_wait | out_wait) {
+      // Up to 4 counters per batch are loaded before any is compared, so
+      // their L2 round trips overlap (a 20-input adder polled one port at a
+      // time waited ~20 sequential round trips per firing).
+      constexpr int kB = 4;
+      for (unsigned pend = in_wait; pend;) {
+        unsigned long long v[kB];
+        int idx[kB], n = 0;
+        for (; pend && n < kB; pend &= pend - 1, ++n) {
+          idx[n] = __ffs(pend) - 1;
+          v[n] = ld_rlx64(&A.in[idx[n]].st->available);
+        }
+        for (int k = 0; k < n; ++k) {
+          const DevChan& c = A.in[idx[k]];
+          if (v[k] >= c.rate)
+            in_wait &= ~(1u << idx[k]);
+          else if (ld_rlx32(&c.st->closed) && ld_rlx64(&c.st->available) < c.rate)
+            stop = true;  // end of stream (read_start -> nullopt)
+        }
+      }
+      for (unsigned pend = out_wait; pend;) {
+        unsigned long long v[kB];
+        int idx[kB], n = 0;
+        for (; pend && n < kB; pend &= pend - 1, ++n) {
+          idx[n] = __ffs(pend) - 1;
+          v[n] = ld_rlx64(&A.out[idx[n]].st->available);
+        }
+        for (int k = 0; k < n; ++k) {
+          const DevChan& c = A.out[idx[k]];
+          if (v[k] + c.rate <= chan_distinct_capacity(c.rate, c.has_delay)) out_wait &= ~(1u << idx[k]);
+        }
+      }
+      if (stop || !(in_wait | out_wait)) break;
+      if (sp.tick(ctl, a) != kOk) {
+        stop = true;
+        *aborted = true;
+      }
+      if (stop) break;
     }
+    __threadfence();
   }
   unsigned wrap = 0;
+  for (unsigned p = 0; !stop && p < A.n_in; ++p)
+    if ((in_on >> p) & 1u)
+      F.in_ptr[p] = A.in[p].storage + chan_read_slot(A.in[p].rate, A.in[p].has_delay, ph.in[p]) * A.in[p].token_size;
   for (unsigned p = 0; !stop && p < A.n_out; ++p) {
     if (!((out_on >> p) & 1u)) continue;
-    const int w = wait_writable(A.out[p], A.out[p].rate, ctl, a, poll);
-    if (w != kOk) {
-      stop = true;
-      *aborted = true;
-    } else {
-      const unsigned ph = A.out[p].st->write_phase;
-      F.out_ptr[p] = A.out[p].storage + chan_write_slot(A.out[p].rate, A.out[p].has_delay, ph) * A.out[p].token_size;
-      if (A.out[p].has_delay && ph % 3 == 2) wrap |= 1u << p;
-    }
+    const unsigned wp = ph.out[p];
+    F.out_ptr[p] = A.out[p].storage + chan_write_slot(A.out[p].rate, A.out[p].has_delay, wp) * A.out[p].token_size;
+    if (A.out[p].has_delay && wp % 3 == 2) wrap |= 1u << p;
   }
   F.firing = i;
   F.stop = stop ? 1u : 0u;
@@ -316,13 +367,33 @@ __device__ float2 poly_sample(float re, float im, int b) {  // poly_branch, dpd.
   return make_float2(__fmul_rn(re, scale), __fmul_rn(im, scale));
 }
 
-__device__ void copy_bytes(unsigned char* dst, const unsigned char* src, unsigned long long n, const Group& G) {
+// Grid-stride loop over [0, n) that issues U independent loads per thread
+// before any store: an actor's few CTAs move a whole token per firing, so
+// memory-level parallelism, not bandwidth, bounds them (one load in flight
+// per thread made the DPD split / source / sink latency-bound).
+template <int U, typename T, typename L, typename S>
+__device__ __forceinline__ void batched(const Group& G, unsigned long long n, L load, S store) {
+  const unsigned long long step = G.step();
+  for (unsigned long long k = G.first(); k < n; k += U * step) {
+    T v[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j)
+      if (k + j * step < n) v[j] = load(k + j * step);
+#pragma unroll
+    for (int j = 0; j < U; ++j)
+      if (k + j * step < n) store(k + j * step, v[j]);
+  }
+}
+
+__device__ __noinline__ void copy_bytes(unsigned char* dst, const unsigned char* src, unsigned long long n, const Group& G) {
   if (((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src) | n) & 15) == 0) {
     const uint4* s = reinterpret_cast<const uint4*>(src);
     uint4* d = reinterpret_cast<uint4*>(dst);
-    for (unsigned long long k = G.first(); k < n / 16; k += G.step()) d[k] = __ldcg(s + k);
+    batched<4, uint4>(G, n / 16, [&](unsigned long long k) { return __ldcg(s + k); },
+                      [&](unsigned long long k, const uint4& v) { d[k] = v; });
   } else {
-    for (unsigned long long k = G.first(); k < n; k += G.step()) dst[k] = __ldcg(src + k);
+    batched<4, unsigned char>(G, n, [&](unsigned long long k) { return __ldcg(src + k); },
+                              [&](unsigned long long k, unsigned char v) { dst[k] = v; });
   }
 }
 
@@ -338,19 +409,29 @@ __device__ void fire_dpd_branch(const ActorDesc& A, const Frame& F, const Group&
   const int T = (int)P.taps_per_branch, H1 = T - 1, b = (int)P.branch;
   const unsigned n = P.period;
   // Chunks of blockDim outputs, round-robin over the group's CTAs; the poly
-  // window (chunk + T-1 history) is staged in shared memory.
-  for (unsigned c0 = G.g * blockDim.x; c0 < n; c0 += G.ctas * blockDim.x) {
-    __syncthreads();
-    for (int w = threadIdx.x; w < (int)blockDim.x + H1; w += blockDim.x) {
-      const long long j = (long long)c0 - H1 + w;
-      float2 u = make_float2(0.f, 0.f);
-      if (j >= 0) {
-        if (j < n) u = poly_sample(__ldcg(re + j), __ldcg(im + j), b);
-      } else {
-        u = __ldcg(state - j - 1);  // FirState x[-(j+1)] (fir10, dpd.cpp:92-97), written by the leader CTA
-      }
-      win[w] = u;
+  // window (chunk + T-1 history) is staged in shared memory.  The raw
+  // inputs of a thread's window positions (w = tid, tid + blockDim) are
+  // loaded one chunk ahead, so each chunk's FIR hides the next loads.
+  const unsigned stride = G.ctas * blockDim.x;
+  auto raw = [&](unsigned c0, int w) -> float2 {
+    const long long j = (long long)c0 - H1 + w;
+    if (w >= (int)blockDim.x + H1 || j >= (long long)n) return make_float2(0.f, 0.f);
+    if (j >= 0) return make_float2(__ldcg(re + j), __ldcg(im + j));
+    return __ldcg(state - j - 1);  // FirState x[-(j+1)] (fir10, dpd.cpp:92-97), written by the leader CTA
+  };
+  float2 nx0 = raw(G.g * blockDim.x, threadIdx.x), nx1 = raw(G.g * blockDim.x, threadIdx.x + blockDim.x);
+  for (unsigned c0 = G.g * blockDim.x; c0 < n; c0 += stride) {
+    const float2 x0 = nx0, x1 = nx1;
+    if (c0 + stride < n) {
+      nx0 = raw(c0 + stride, threadIdx.x);
+      nx1 = raw(c0 + stride, threadIdx.x + blockDim.x);
     }
+    __syncthreads();
+    // poly of the raw samples; history positions before the block start are
+    // already poly outputs (the FirState).
+    const long long j0 = (long long)c0 - H1 + threadIdx.x, j1 = j0 + blockDim.x;
+    win[threadIdx.x] = j0 >= 0 ? poly_sample(x0.x, x0.y, b) : x0;
+    if ((int)threadIdx.x < H1) win[threadIdx.x + blockDim.x] = j1 >= 0 ? poly_sample(x1.x, x1.y, b) : x1;
     __syncthreads();
     const unsigned o = c0 + threadIdx.x;
     if (o < n) {
@@ -393,11 +474,11 @@ __device__ void fire_kind(const ActorDesc& A, const Frame& F, const Group& G, Ac
       const float2* x = reinterpret_cast<const float2*>(P.samples) + F.firing * P.period;
       float* re = reinterpret_cast<float*>(F.out_ptr[0]);
       float* im = reinterpret_cast<float*>(F.out_ptr[1]);
-      for (unsigned long long s = G.first(); s < P.period; s += G.step()) {
-        const float2 v = x[s];
-        re[s] = v.x;
-        im[s] = v.y;
-      }
+      batched<4, float2>(G, P.period, [&](unsigned long long k) { return x[k]; },
+                         [&](unsigned long long k, const float2& v) {
+                           re[k] = v.x;
+                           im[k] = v.y;
+                         });
       break;
     }
     case DF_ACT_DPD_SINK: {  // dpd.cpp:333-347
@@ -405,7 +486,8 @@ __device__ void fire_kind(const ActorDesc& A, const Frame& F, const Group& G, Ac
       float2* y = reinterpret_cast<float2*>(P.samples) + F.firing * P.period;
       const float* re = reinterpret_cast<const float*>(F.in_ptr[0]);
       const float* im = reinterpret_cast<const float*>(F.in_ptr[1]);
-      for (unsigned long long s = G.first(); s < P.period; s += G.step()) y[s] = make_float2(__ldcg(re + s), __ldcg(im + s));
+      batched<4, float2>(G, P.period, [&](unsigned long long k) { return make_float2(__ldcg(re + k), __ldcg(im + k)); },
+                         [&](unsigned long long k, const float2& v) { y[k] = v; });
       break;
     }
     case DF_ACT_DPD_CONFIG: {  // dpd.cpp:206-221: the same LE token on every output
@@ -430,15 +512,29 @@ __device__ void fire_kind(const ActorDesc& A, const Frame& F, const Group& G, Ac
       const unsigned n = (unsigned)(A.out[0].token_size / 4) * A.out[0].rate;
       float* ore = reinterpret_cast<float*>(F.out_ptr[0]);
       float* oim = reinterpret_cast<float*>(F.out_ptr[1]);
-      for (unsigned long long s = G.first(); s < n; s += G.step()) {
-        float r = 0.0f, i = 0.0f;
+      for (unsigned long long s0 = G.first(); s0 < n; s0 += 2 * G.step()) {
+        // two outputs per iteration: their loads are independent
+        const unsigned long long s1 = s0 + G.step();
+        const bool two = s1 < n;
+        float r0 = 0.0f, i0 = 0.0f, r1 = 0.0f, i1 = 0.0f;
+#pragma unroll 1
         for (unsigned p = 0; p + 1 < A.n_in; p += 2) {
           if (!((F.in_on >> p) & 1u)) continue;
-          r = __fadd_rn(r, __ldcg(reinterpret_cast<const float*>(F.in_ptr[p]) + s));
-          i = __fadd_rn(i, __ldcg(reinterpret_cast<const float*>(F.in_ptr[p + 1]) + s));
+          const float* pr = reinterpret_cast<const float*>(F.in_ptr[p]);
+          const float* pi = reinterpret_cast<const float*>(F.in_ptr[p + 1]);
+          const float a0 = __ldcg(pr + s0), b0 = __ldcg(pi + s0);
+          const float a1 = two ? __ldcg(pr + s1) : 0.f, b1 = two ? __ldcg(pi + s1) : 0.f;
+          r0 = __fadd_rn(r0, a0);
+          i0 = __fadd_rn(i0, b0);
+          r1 = __fadd_rn(r1, a1);
+          i1 = __fadd_rn(i1, b1);
         }
-        ore[s] = r;
-        oim[s] = i;
+        ore[s0] = r0;
+        oim[s0] = i0;
+        if (two) {
+          ore[s1] = r1;
+          oim[s1] = i1;
+        }
       }
       break;
     }
@@ -505,9 +601,20 @@ __device__ void fire_kind(const ActorDesc& A, const Frame& F, const Group& G, Ac
     case DF_ACT_THRES: {  // thres_diff (motion.cpp:50-57): in0 prev, in1 cur
       const df_act_frames& P = params<df_act_frames>(A);
       const unsigned long long total = (unsigned long long)A.in[0].rate * A.in[0].token_size;
-      for (unsigned long long k = G.first(); k < total; k += G.step()) {
-        const int d = (int)__ldcg(F.in_ptr[1] + k) - (int)__ldcg(F.in_ptr[0] + k);
-        F.out_ptr[0][k] = (d < 0 ? -d : d) > (int)P.threshold ? 255 : 0;
+      if (((reinterpret_cast<uintptr_t>(F.in_ptr[0]) | reinterpret_cast<uintptr_t>(F.in_ptr[1]) |
+            reinterpret_cast<uintptr_t>(F.out_ptr[0]) | total) & 3) == 0) {
+        // 4 px per word: |cur - prev| per byte (VABSDIFF4), > thr per byte -> 0xFF
+        const unsigned* prev = reinterpret_cast<const unsigned*>(F.in_ptr[0]);
+        const unsigned* cur = reinterpret_cast<const unsigned*>(F.in_ptr[1]);
+        unsigned* out = reinterpret_cast<unsigned*>(F.out_ptr[0]);
+        const unsigned thr4 = 0x01010101u * P.threshold;
+        batched<4, uint2>(G, total / 4, [&](unsigned long long k) { return make_uint2(__ldcg(prev + k), __ldcg(cur + k)); },
+                          [&](unsigned long long k, const uint2& v) { out[k] = __vcmpgtu4(__vabsdiffu4(v.y, v.x), thr4); });
+      } else {
+        for (unsigned long long k = G.first(); k < total; k += G.step()) {
+          const int d = (int)__ldcg(F.in_ptr[1] + k) - (int)__ldcg(F.in_ptr[0] + k);
+          F.out_ptr[0][k] = (d < 0 ? -d : d) > (int)P.threshold ? 255 : 0;
+        }
       }
       break;
     }
@@ -566,23 +673,25 @@ __device__ void post_kind(const ActorDesc& A, const Frame& F, ActorRt* rt) {
 // Leader, after the loop: close outputs, then drain inputs until their
 // producers close (runtime.cpp:223-229, drain_channel :199-204).
 __device__ void leader_finish(const ActorDesc& A, int a, ActorRt* rt, NetCtl* ctl, bool aborted,
-                              unsigned long long* poll) {
+                              unsigned long long* poll, Phases& ph) {
   rt->t_stop = now_ns();
   for (unsigned p = 0; p < A.n_out; ++p) close_channel(A.out[p]);
   if (aborted) return;
-  auto drain = [&](const DevChan& c) {
-    while (wait_readable(c, c.rate, ctl, a, poll) == kOk) commit_read(c, c.rate);
+  auto drain = [&](const DevChan& c, unsigned& phase) {  // discards: nothing is read before the release
+    while (wait_readable(c, c.rate, ctl, a, poll) == kOk) commit_read(c, c.rate, phase);
   };
-  for (unsigned p = 0; p < A.n_in; ++p) drain(A.in[p]);
-  if (A.has_ctrl) drain(A.ctrl);
+  for (unsigned p = 0; p < A.n_in; ++p) drain(A.in[p], ph.in[p]);
+  if (A.has_ctrl) drain(A.ctrl, ph.ctrl);
 }
 
-__global__ void __launch_bounds__(kNetThreads) net_kernel(const ActorDesc* __restrict__ actors, unsigned n_actors,
+__global__ void __launch_bounds__(kNetThreads, 4) net_kernel(const ActorDesc* __restrict__ actors, unsigned n_actors,
                                                           ActorRt* rts, NetCtl* ctl) {
   __shared__ int s_actor;
   __shared__ Frame s_frame;
   __shared__ float2 win[kNetThreads + 32];
   __shared__ bool s_aborted;
+  __shared__ Phases s_ph;  // leader CTA: the actor's endpoint phases
+  __shared__ unsigned long long s_t;  // leader: timestamp of the current phase
   if (threadIdx.x == 0) {
     s_actor = -1;
     for (unsigned a = 0; a < n_actors; ++a)
@@ -596,14 +705,24 @@ __global__ void __launch_bounds__(kNetThreads) net_kernel(const ActorDesc* __res
   ActorRt* rt = rts + a;
   const Group G{blockIdx.x - A.cta0, A.ctas};
   const bool leader_cta = G.g == 0;
+  if (leader_cta && threadIdx.x < kMaxPorts) {
+    s_ph.in[threadIdx.x] = threadIdx.x < A.n_in ? A.in[threadIdx.x].st->read_phase : 0;
+    s_ph.out[threadIdx.x] = threadIdx.x < A.n_out ? A.out[threadIdx.x].st->write_phase : 0;
+    if (threadIdx.x == 0) s_ph.ctrl = A.has_ctrl ? A.ctrl.st->read_phase : 0;
+  }
+  __syncthreads();
   unsigned gen = 0;
   unsigned long long host_poll = 0;  // leader thread: last poll of the host abort word
   for (;;) {
     if (threadIdx.x == 0) {
       if (leader_cta) {
         bool ab = false;
-        leader_prepare(A, a, rt, ctl, &ab, &host_poll);
+        const unsigned long long t0 = now_ns();
+        leader_prepare(A, a, rt, ctl, &ab, &host_poll, s_ph);
         s_aborted = ab;
+        const unsigned long long t1 = now_ns();
+        rt->t_wait += t1 - t0;
+        s_t = t1;
       } else {
         Spin s;
         s.watchdog = false;  // the leader's own waits carry the watchdog
@@ -644,6 +763,9 @@ __global__ void __launch_bounds__(kNetThreads) net_kernel(const ActorDesc* __res
         }
       rt->done = 0;
       s_aborted = ab;
+      const unsigned long long t = now_ns();
+      rt->t_fire += t - s_t;
+      s_t = t;
     }
     __syncthreads();
     if (s_aborted) break;
@@ -655,17 +777,22 @@ __global__ void __launch_bounds__(kNetThreads) net_kernel(const ActorDesc* __res
         copy_bytes(c.storage, c.storage + 3ull * c.rate * c.token_size, c.token_size, Group{0, 1});
       }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    // write_end / read_end of every port at once: lane p of warp 0 commits
+    // output p and input p (each lane fences its own view first), instead
+    // of one thread walking up to 48 ports.
+    if (threadIdx.x < 32) {
+      const unsigned p = threadIdx.x;
       __threadfence();
-      for (unsigned p = 0; p < A.n_out; ++p)
-        if ((s_frame.out_on >> p) & 1u) commit_write(A.out[p], A.out[p].rate);
-      for (unsigned p = 0; p < A.n_in; ++p)
-        if ((s_frame.in_on >> p) & 1u) commit_read(A.in[p], A.in[p].rate);
-      ++rt->firings;
+      if (p < A.n_out && ((s_frame.out_on >> p) & 1u)) commit_write(A.out[p], A.out[p].rate, s_ph.out[p]);
+      if (p < A.n_in && ((s_frame.in_on >> p) & 1u)) commit_read(A.in[p], A.in[p].rate, s_ph.in[p]);
+      if (p == 0) {
+        ++rt->firings;
+        rt->t_commit += now_ns() - s_t;
+      }
     }
   }
   if (leader_cta && threadIdx.x == 0)
-    leader_finish(A, a, rt, ctl, s_aborted || *(volatile unsigned*)&ctl->abort, &host_poll);
+    leader_finish(A, a, rt, ctl, s_aborted || *(volatile unsigned*)&ctl->abort, &host_poll, s_ph);
 }
 
 }  // namespace
@@ -951,6 +1078,16 @@ int df_net_fault(const df_net* n, int* actor, int* code, uint32_t* token) {
   if (actor) *actor = n->ctl.fault_code ? (int)n->ctl.fault_actor : -1;
   if (code) *code = (int)n->ctl.fault_code;
   if (token) *token = n->ctl.fault_token;
+  return DF_OK;
+}
+
+int df_net_actor_profile(const df_net* n, int actor, double* wait_ms, double* fire_ms, double* commit_ms) {
+  DF_REQUIRE(n && actor >= 0 && (size_t)actor < n->actors.size(), DF_EINVAL, "df_net_actor_profile: no such actor");
+  DF_REQUIRE(n->ran && n->rt.size() == n->actors.size(), DF_ELOGIC, "df_net_actor_profile: the network has not run");
+  const ActorRt& r = n->rt[actor];
+  if (wait_ms) *wait_ms = (double)r.t_wait / 1e6;
+  if (fire_ms) *fire_ms = (double)r.t_fire / 1e6;
+  if (commit_ms) *commit_ms = (double)r.t_commit / 1e6;
   return DF_OK;
 }
 

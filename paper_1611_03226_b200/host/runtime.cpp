@@ -11,6 +11,8 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <functional>
@@ -242,11 +244,18 @@ RunStats run_device(const NetworkGraph& net, const ExecutionConfig& cfg, std::ch
     if (!who.empty()) throw ActorFault(who, e.what());
     throw;
   }
+  const bool profile = std::getenv("DF_NET_PROFILE") != nullptr;
   for (std::size_t a = 0; a < net.actors().size(); ++a) {
     std::uint64_t firings = 0;
     double ms = 0.0;
     df_net_actor_stats(dn, static_cast<int>(a), &firings, &ms);
     stats.actors.push_back({net.actors()[a].id, firings, ms});
+    if (profile) {  // tracing aid: where each actor's leader spent its time
+      double w = 0, f = 0, c = 0;
+      df_net_actor_profile(dn, static_cast<int>(a), &w, &f, &c);
+      std::fprintf(stderr, "df_net %-10s firings %8llu active %9.3f ms  wait %9.3f  fire %9.3f  commit %9.3f ms\n",
+                   net.actors()[a].id.c_str(), (unsigned long long)firings, ms, w, f, c);
+    }
   }
   if (cfg.stats_enabled)
     for (std::size_t c = 0; c < chans.size(); ++c) {

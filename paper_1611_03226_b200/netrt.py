@@ -75,6 +75,12 @@ class Net:
         call("df_net_actor_stats", self.handle, actor, C.byref(f), C.byref(ms))
         return f.value, ms.value
 
+    def profile(self, actor: int):
+        """(wait_ms, fire_ms, commit_ms) of the actor's leader over the run."""
+        w, f, c = C.c_double(), C.c_double(), C.c_double()
+        call("df_net_actor_profile", self.handle, actor, C.byref(w), C.byref(f), C.byref(c))
+        return w.value, f.value, c.value
+
     def close(self):
         if self.handle:
             lib().df_net_destroy(self.handle)
