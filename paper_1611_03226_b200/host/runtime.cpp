@@ -20,6 +20,7 @@
 #include <sstream>
 
 #include "df_cuda.h"
+#include "nvtx3/nvToolsExt.h"  // header-only NVTX v3: ranges per firing / run (no-ops without a tool)
 
 namespace df {
 
@@ -213,7 +214,9 @@ RunStats run_device(const NetworkGraph& net, const ExecutionConfig& cfg, std::ch
       if (spec.behavior.init) spec.behavior.init();
     }
     fault_actor.clear();
+    nvtxRangePushA("df_net_run (device-resident network)");
     const int rc = df_net_run(dn, cfg.device_timeout_s);
+    nvtxRangePop();
     if (rc != DF_OK) {
       const std::string detail = df_last_error();
       int who = -1, code = 0;
@@ -378,10 +381,12 @@ RunStats run(const NetworkGraph& net, const ExecutionConfig& cfg) {
         if (i == 0) check(df_event_record(r.t_first, r.stream));
         r.ctx.reset(i, r.stream, cfg.device);
         fault_actor = r.spec->id;
+        nvtxRangePushA(r.spec->id.c_str());  // the enqueue of firing i (host timeline)
         if (r.spec->behavior.is_host())
           fire_host_actor(r, i, host_faults, host_jobs);
         else
           r.spec->behavior.fire(r.ctx);
+        nvtxRangePop();
         fault_actor.clear();
         check(df_event_record(r.done[i % 3], r.stream));
         ++r.firings;
