@@ -257,7 +257,9 @@ def bench_motion_ours(args, p, rank, world, local):
     launches0 = device.kernel_launches()
     if world == 1:
         # The K timed steps are captured in ONE CUDA graph so host-side
-        # enqueue latency never starves the device between steps.
+        # enqueue latency never starves the device between steps; it is
+        # replayed once untimed first (warm-up that also keeps the device
+        # busy while the timed replay is submitted).
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
             for _ in range(args.steps):
@@ -266,6 +268,8 @@ def bench_motion_ours(args, p, rank, world, local):
     launches = device.kernel_launches() - launches0
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
+        if graph is not None:
+            graph.replay()
         t0.record(stream)
         if graph is not None:
             graph.replay()
@@ -383,11 +387,20 @@ def bench_dpd_ours(args, p, rank, world, local):
     sched = dpd_schedule(p["sched"], blocks)
     stream = torch.cuda.current_stream()
     sh = C.c_void_p(stream.cuda_stream)
-    x_buf = device.Buffer(8 * N, local)  # cudaMalloc'ed: exportable to the neighbour rank
-    x = x_buf.as_tensor(np.float32)
-    y = torch.empty(2 * N, dtype=torch.float32, device=dev)
+    # Input + output smaller than L2 (DPD-1: 16 MB vs 126 MB): consecutive
+    # steps fire on a rotating pool of R input/output batches whose total
+    # exceeds L2, so every step reads a batch last touched R-1 steps
+    # (>= 256 MB of traffic) earlier -- cold, as a streaming actor sees it --
+    # and K steps run back to back between one event pair (per-step event
+    # pairs around a flushed step add ~6 us of event-node overhead to a
+    # ~12 us firing: tools/probe_event_overhead.py, profiles/r02_dpd_timing.txt).
+    R = max(1, -(-L2_FLUSH_BYTES // (16 * N)))
+    x_buf = device.Buffer(8 * N * R, local)  # cudaMalloc'ed: exportable to the neighbour rank
+    x_pool = x_buf.as_tensor(np.float32)
+    y_pool = torch.empty(2 * N * R, dtype=torch.float32, device=dev)
+    x, y = x_pool[: 2 * N], y_pool[: 2 * N]
     ctrl = torch.empty(blocks, dtype=torch.int32, device=dev)
-    _lib.call("df_fill_random_pm1", C.c_void_p(x.data_ptr()), 2 * N, 99 + rank, sh)
+    _lib.call("df_fill_random_pm1", C.c_void_p(x_pool.data_ptr()), 2 * N * R, 99 + rank, sh)
     taps = np.random.default_rng(808).uniform(-0.5, 0.5, size=(10, T, 2)).astype(np.float32)
     actor = dpd.DpdActor(period, taps, device=local)
     sched_np = np.ascontiguousarray(sched)
@@ -423,85 +436,78 @@ def bench_dpd_ours(args, p, rank, world, local):
         # The global stream is the ranks' shards back to back (the schedule
         # cycling over global block indices), so each branch's halo is
         # the tail of its last active block before this shard, on whichever
-        # lower rank holds it (shard.dpd_halo_tails).
+        # lower rank holds it (shard.dpd_halo_tails).  Pool slot k of every
+        # rank holds the same step, so slot k's tails sit k*8N bytes further.
         ranges = [(r * N, (r + 1) * N) for r in range(world)]
         tails_g = shard.dpd_halo_tails(sched, ranges, period, T, rank, peer.peers)  # global block indices
-        tail_ptrs = (C.c_void_p * 10)(*[C.c_void_p(t) if t is not None else None for t in tails_g])
+        tail_ptrs = [(C.c_void_p * 10)(*[C.c_void_p(t + 8 * N * k) if t is not None else None for t in tails_g])
+                     for k in range(R)]
 
-    def step(ev0=None, ev1=None):
+    def step(i=0):
         sh = C.c_void_p(torch.cuda.current_stream().cuda_stream)  # the capture stream inside a graph
+        k = i % R
+        xk, yk = x_pool[2 * N * k: 2 * N * (k + 1)], y_pool[2 * N * k: 2 * N * (k + 1)]
         if world > 1 and HALO != "ipc":  # NCCL P2P variant: exchange the tails, set the histories
             for b, hb in enumerate(tail_src):
                 if hb is not None:
                     a0 = 2 * ((hb + 1) * period - H1)
-                    tails[2 * H1 * b: 2 * H1 * (b + 1)].copy_(x[a0: a0 + 2 * H1])
+                    tails[2 * H1 * b: 2 * H1 * (b + 1)].copy_(xk[a0: a0 + 2 * H1])
             if shard.exchange_tail(tails, halo, rank, world):
                 for b in range(10):
                     _lib.call("df_dpd_set_history", actor.handle, C.c_void_p(halo.data_ptr() + 8 * H1 * b), H1,
                               1 << b, sh)
-        if ev0 is not None:
-            ev0.record(torch.cuda.current_stream())
         if tail_ptrs is not None:
-            _lib.call("df_dpd_fire_halo", actor.handle, tail_ptrs, C.c_void_p(ctrl.data_ptr()),
-                      C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), blocks, sh)
+            _lib.call("df_dpd_fire_halo", actor.handle, tail_ptrs[k], C.c_void_p(ctrl.data_ptr()),
+                      C.c_void_p(xk.data_ptr()), C.c_void_p(yk.data_ptr()), blocks, sh)
         else:
-            _lib.call("df_dpd_fire", actor.handle, C.c_void_p(ctrl.data_ptr()), C.c_void_p(x.data_ptr()),
-                      C.c_void_p(y.data_ptr()), blocks, sh)
-        if ev1 is not None:
-            ev1.record(torch.cuda.current_stream())
+            _lib.call("df_dpd_fire", actor.handle, C.c_void_p(ctrl.data_ptr()), C.c_void_p(xk.data_ptr()),
+                      C.c_void_p(yk.data_ptr()), blocks, sh)
 
-    for _ in range(args.warmup):
-        step()
+    # Warm-up walks the whole pool once (first touch of every batch).
+    for i in range(max(args.warmup, R)):
+        step(i)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    graph = None
-    # Input + output smaller than L2 (DPD-1: 16 MB vs 126 MB): a step would
-    # find the previous step's input still L2-resident, so every timed
-    # step is preceded by an L2 flush (a 256 MB write, outside that step's
-    # events) and timed alone; value and ms_per_step are the per-step
-    # event times.
-    l2_flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev) if 16 * N < L2_FLUSH_BYTES else None
-    launches0 = device.kernel_launches()
-    # Per-step events; captured into the graph as event-record nodes
-    # (external) when the steps are flushed and timed one by one.
-    kev = [(torch.cuda.Event(enable_timing=True, external=True), torch.cuda.Event(enable_timing=True, external=True))
-           for _ in range(args.steps)]
+    graph = lead = None
     if world == 1 or HALO == "ipc":
         # K steps, one graph (see bench_motion_ours).  At N > 1 the IPC
         # transport needs no per-step communication (the firing reads its
         # halo over NVLink), so the steps are pure launches and capture too.
+        # `lead` is K untimed steps replayed just before the timed graph so
+        # the device is busy while the timed graph is submitted; the timed
+        # steps continue the pool rotation after it (steps K..2K-1).
+        lead = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(lead):
+            for i in range(args.steps):
+                step(i)
+        launches0 = device.kernel_launches()
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
-            for i in range(args.steps):
-                if l2_flush is not None:
-                    l2_flush.fill_(i & 0xFF)
-                    step(*kev[i])
-                else:
-                    step()
+            for i in range(args.steps, 2 * args.steps):
+                step(i)
+        launches = device.kernel_launches() - launches0
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-    launches = device.kernel_launches() - launches0
+    else:
+        launches0 = device.kernel_launches()
     with ClockSampler(local) as clk:
+        if lead is not None:
+            lead.replay()
         t0.record(stream)
         if graph is not None:
             graph.replay()
         else:
-            for i in range(args.steps):
-                if l2_flush is not None:
-                    l2_flush.fill_(i & 0xFF)
-                step(*kev[i])
+            for i in range(args.steps, 2 * args.steps):
+                step(i)
         t1.record(stream)
         torch.cuda.synchronize()
     if graph is None:
         launches = device.kernel_launches() - launches0
     ms = max_over_ranks(t0.elapsed_time(t1) / args.steps, world)
-    kms = ms if graph is not None and l2_flush is None else max_over_ranks(
-        statistics.mean(a.elapsed_time(b) for a, b in kev), world)
-    if l2_flush is not None:
-        ms = kms  # the flushes between steps are not part of the step
+    kms = ms
     actor.check()
 
     hin = device.PinnedArray(2 * N, np.float32)
@@ -534,8 +540,9 @@ def bench_dpd_ours(args, p, rank, world, local):
                    "parallelism": f"block-range shards x{world}, per-branch FIR-history halo via "
                                   + ("in-kernel NVLink peer reads (CUDA IPC)" if HALO == "ipc" else "NCCL P2P"),
                    "l2": f"in+out {16 * N / 1e6:.0f} MB per GPU"
-                         + (f" < L2: {L2_FLUSH_BYTES >> 20} MB L2 flush before every timed step (outside its events)"
-                            if l2_flush is not None else " > 126 MB L2 (no flush needed)")},
+                         + (f" < L2: steps rotate over {R} input/output batches ({16 * N * R >> 20} MB > 126 MB L2), "
+                            "so every step's input is cold; K steps back to back, one event pair"
+                            if R > 1 else " > 126 MB L2 (no flush needed)")},
         "e2e": {"value": round(world * N / e2e_s / 1e6, 1), "unit": "Msamples/s",
                 "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * N,
                 "path": "df_dpd_run_host (C ABI, pinned host buffers)"},

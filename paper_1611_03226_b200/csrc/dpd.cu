@@ -55,6 +55,38 @@ namespace {
 constexpr int kBranches = 10;
 constexpr int kMaxTaps = 32;
 
+// DF_DPD_TRACE (probe builds only, tools/probe_dpd_trace.py): %globaltimer
+// stamps per tile warp -- start, window loaded, FIR done, end -- stored at a
+// deterministic slot (no atomics on the warp's critical path).
+#ifdef DF_DPD_TRACE
+__device__ unsigned long long g_dpd_trace[8 << 15];
+__device__ __forceinline__ unsigned long long dpd_gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void dpd_trace(unsigned slot, unsigned long long id, unsigned long long t0,
+                                          unsigned long long t1, unsigned long long tf) {
+  const unsigned long long t2 = dpd_gtime();
+  if (slot < (1u << 15)) {
+    unsigned sm, ws;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    asm volatile("mov.u32 %0, %%warpid;" : "=r"(ws));
+    g_dpd_trace[8 * slot] = id | ((unsigned long long)sm << 40) | ((unsigned long long)ws << 56);
+    g_dpd_trace[8 * slot + 1] = t0;
+    g_dpd_trace[8 * slot + 2] = t1;
+    g_dpd_trace[8 * slot + 3] = t2;
+    g_dpd_trace[8 * slot + 4] = tf;
+  }
+}
+#define DPD_TSTAMP(v) const unsigned long long v = dpd_gtime()
+#define DPD_TRACE(slot, id, a, b, f) \
+  if ((threadIdx.x & 31) == 0) dpd_trace(slot, id, a, b, f)
+#else
+#define DPD_TSTAMP(v)
+#define DPD_TRACE(slot, id, a, b, f)
+#endif
+
 struct DpdIO {
   // Raw mode: direct pointers.  Channel mode: resolved from the device
   // phases at kernel start (chan_*_region) -- the host never learns them.
@@ -276,6 +308,7 @@ __global__ void __launch_bounds__(THREADS, dpd_min_blocks<T>()) dpd_main_kernel(
   float2* __restrict__ y = io_out(io);
 
   const int tid = threadIdx.x;
+  DPD_TSTAMP(tr_start);
   // L2 prefetch of the input tile of the CTA dispatched `ahead` (= the
   // resident CTA slots) after this one: it starts about when this CTA
   // retires, and finds its input in L2 instead of waiting on HBM.
@@ -335,6 +368,7 @@ __global__ void __launch_bounds__(THREADS, dpd_min_blocks<T>()) dpd_main_kernel(
     mg[m] = __fsqrt_rn(__fadd_rn(__fmul_rn(xr[m], xr[m]), __fmul_rn(xi[m], xi[m])));
     sc[m] = 1.0f;
   }
+  DPD_TSTAMP(tr_loaded);
 
   // Branch sum starts at -0.0f, the exact additive identity (-0 + x == x
   // for every x, including +0): the first add reproduces y_b bit for bit,
@@ -469,6 +503,7 @@ __global__ void __launch_bounds__(THREADS, dpd_min_blocks<T>()) dpd_main_kernel(
   }
 
   // Stage through smem for coalesced stores (reuse the idle buffer).
+  DPD_TSTAMP(tr_fir);
   if (C::WL)
     __syncwarp();
   else
@@ -484,6 +519,8 @@ __global__ void __launch_bounds__(THREADS, dpd_min_blocks<T>()) dpd_main_kernel(
       const int o = lt + 32 * i;
       if (wb + o < n) y[blk + t0 + wb + o] = st[pad_index(o)];
     }
+    DPD_TRACE((unsigned)((blockIdx.x + (unsigned long long)blockIdx.y * gridDim.x) * (THREADS / 32) + (tid >> 5)),
+              p * 65536ull + tile * 4 + (tid >> 5), tr_start, tr_loaded, tr_fir);
   } else {
     __syncthreads();
     for (int o = tid; o < n; o += THREADS) y[blk + t0 + o] = st[pad_index(o)];
@@ -895,6 +932,18 @@ int df_dpd_set_history(df_dpd* d, const float* raw_dev, uint32_t count, uint32_t
                                                                    count, branch_mask, (int)d->T);
   return after_launch("dpd_set_history_kernel");
 }
+
+#ifdef DF_DPD_TRACE
+// Probe builds only: copies out (and clears) the trace slots.
+int df_debug_dpd_trace(unsigned long long* host, unsigned* count) {
+  DF_CHECK_CUDA(cudaDeviceSynchronize());
+  if (host) DF_CHECK_CUDA(cudaMemcpyFromSymbol(host, g_dpd_trace, (8ull << 15) * 8));
+  *count = 1u << 15;
+  static std::vector<unsigned long long> zeros(8 << 15);
+  DF_CHECK_CUDA(cudaMemcpyToSymbol(g_dpd_trace, zeros.data(), (8ull << 15) * 8));
+  return DF_OK;
+}
+#endif
 
 int df_dpd_fire(df_dpd* d, const uint32_t* ctrl_dev, const float* in_dev, float* out_dev,
                 uint64_t blocks, void* stream) {

@@ -44,14 +44,18 @@ def test_default_run_is_n1_motion720():
 
 def test_l2_rule_every_workload_flushes_or_exceeds_l2():
     """Timing rule: between timed steps either flush L2 or use data larger
-    than L2 (126 MB).  DPD workloads below L2_FLUSH_BYTES are flushed; every
-    other workload's input alone exceeds L2."""
+    than L2 (126 MB).  DPD workloads whose in+out is below L2_FLUSH_BYTES
+    rotate over a pool of batches larger than L2 (every step reads a cold
+    batch); every other workload's input alone exceeds L2."""
     l2 = 126e6
     assert bench.L2_FLUSH_BYTES > l2
+    src = open(bench.__file__).read()
+    assert "R = max(1, -(-L2_FLUSH_BYTES // (16 * N)))" in src
     for name, (kind, p) in bench.WORKLOADS.items():
         if kind == "dpd":
-            flushed = 16 * p["samples"] < bench.L2_FLUSH_BYTES
-            assert flushed or 8 * p["samples"] > l2, name
-            assert flushed == (name == "dpd1"), name
+            pooled = 16 * p["samples"] < bench.L2_FLUSH_BYTES
+            R = max(1, -(-bench.L2_FLUSH_BYTES // (16 * p["samples"])))
+            assert 16 * p["samples"] * R > l2, name
+            assert pooled == (name == "dpd1") == (R > 1), name
         else:
             assert p["w"] * p["h"] * p["fmt"] * p["frames"] > l2, name
