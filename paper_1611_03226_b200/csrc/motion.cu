@@ -608,6 +608,9 @@ constexpr size_t kSmemBytes = sizeof(uint2) * kWarpsPerCta * (kBandRows + 2) * 3
 #ifndef DF_M3_EARLY_MIN_R
 #define DF_M3_EARLY_MIN_R 59
 #endif
+#ifndef DF_M3_ALT
+#define DF_M3_ALT 1  // odd temporal chunks walk backwards (shared boundary frames hit L2)
+#endif
 constexpr int kM3Warps = 4;
 // Band heights R (template parameter): a frame pass fetches rows y0-3 ..
 // y0+R+2 (R + 6 rows, whole 5-row boxes), gauss(prev) holds R + 2 rows in
@@ -731,6 +734,7 @@ struct M3Stream {
   unsigned cur;       // this lane's bytes in the current group's first row
   int c0;             // tensor column (uint32 units) of the warp tile
   int fs, H, y0;
+  int dir;            // +1: pass P reads frame fs + P; -1: frame fs - P (backward chunk)
   int lane;
 
   __device__ __forceinline__ void issue(unsigned gi, unsigned s) {  // lane 0 only
@@ -740,10 +744,10 @@ struct M3Stream {
     mbar_expect_tx(bars + 8 * s, kM3RPS * m3_row_bytes<FMT>());
     const CUtensorMap* m = (hfirst && pass == 0) ? hmap : map;
 #if DF_M3_TMA3D
-    const int f = (hfirst && pass == 0) ? 0 : fs + (int)pass;
+    const int f = (hfirst && pass == 0) ? 0 : fs + dir * (int)pass;
 #else  // A/B baseline: frames stacked on the row axis (frame f at row f*H)
     const int f = 0;
-    row += (hfirst && pass == 0) ? 0 : (fs + (int)pass) * H;
+    row += (hfirst && pass == 0) ? 0 : (fs + dir * (int)pass) * H;
 #endif
     const unsigned in_pass = gi % GPP;
     if (l2hint && in_pass < 2)
@@ -786,8 +790,9 @@ struct M3Row {
   unsigned t[2];  // threshold flags
 };
 
-// One frame pass (MODE 0 warm-up / 1 chain / 2 chain + delay token) of the
-// warp's (tile, band).  INT: interior band (no border rows, full R rows).
+// One frame pass (MODE 0 warm-up / 1 chain / 2 chain + delay token / 3
+// warm-up + delay token) of the warp's (tile, band).  INT: interior band (no
+// border rows, full R rows).
 template <int FMT, int R, int MODE, bool INT>
 __device__ __forceinline__ void m3_pass(M3Stream<FMT, R>& st, unsigned char* __restrict__ out,
                                         unsigned char* __restrict__ next_tok, unsigned char* __restrict__ next_copy,
@@ -800,7 +805,9 @@ __device__ __forceinline__ void m3_pass(M3Stream<FMT, R>& st, unsigned char* __r
   // Each prev row is read (tcgen05.ld, waited) before it is overwritten in
   // the same step; the previous pass's stores must have landed before this
   // pass's loads.
-  if (MODE != 0) tmem_wait_st();
+  constexpr bool CHAIN = MODE == 1 || MODE == 2;  // thres + median against TMEM's prev
+  constexpr bool TOK = MODE == 2 || MODE == 3;    // this pass's gauss is the next delay token
+  if (CHAIN) tmem_wait_st();
 
   // Row k (0..4) of the current group: the group is acquired at k == 0 and
   // released at k == 4.  fetch() reads the row's words from the ring;
@@ -841,7 +848,7 @@ __device__ __forceinline__ void m3_pass(M3Stream<FMT, R>& st, unsigned char* __r
   auto gauss_thres = [&](M3Row& r4, M3Row& r3, M3Row& r2, M3Row& r1, M3Row& r0, int gc) {
     const unsigned ta = tmem + 2u * (unsigned)(gc - (y0 - 1));
     unsigned p0 = 0, p1 = 0;
-    if (MODE != 0) tmem_ld2(ta, p0, p1);
+    if (CHAIN) tmem_ld2(ta, p0, p1);
     unsigned gw[2];
     if (!INT && (unsigned)(gc - 2) >= (unsigned)(H - 4)) {  // gc < 2 || gc >= H-2: gray copied
       gw[0] = r2.g[0];
@@ -855,13 +862,13 @@ __device__ __forceinline__ void m3_pass(M3Stream<FMT, R>& st, unsigned char* __r
         gw[w] = lop_sel(gm[w], r2.g[w], prmt(v0, v1, 0x7531));
       }
     }
-    if (MODE != 0) {
+    if (CHAIN) {
       tmem_wait_ld(p0, p1);
       r2.t[0] = thres4(gw[0], p0, g);
       r2.t[1] = thres4(gw[1], p1, g);
     }
     tmem_st2(ta, gw[0], gw[1]);
-    if (MODE == 2 && out_lane && x < W && gc >= y0 && gc < y0 + R && gc < H) {
+    if (TOK && out_lane && x < W && gc >= y0 && gc < y0 + R && gc < H) {
       const unsigned o = (unsigned)gc * (unsigned)W + (unsigned)x;
       *reinterpret_cast<uint2*>(next_tok + o) = make_uint2(gw[0], gw[1]);
       if (next_copy) *reinterpret_cast<uint2*>(next_copy + o) = make_uint2(gw[0], gw[1]);  // Fig. 2 phase 2
@@ -896,11 +903,11 @@ __device__ __forceinline__ void m3_pass(M3Stream<FMT, R>& st, unsigned char* __r
       uint2 w[3] = {};
       if (gc < gc_end) fetch(k, w);
       gauss_thres(r4, r3, r2, r1, r0, gc);
-      if (MODE != 0 && gc > y0) median(r4, r3, r2, gc - 1);
+      if (CHAIN && gc > y0) median(r4, r3, r2, gc - 1);
       if (gc < gc_end) finish(r4, k, w);
     } else {
       gauss_thres(r4, r3, r2, r1, r0, gc);
-      if (MODE != 0 && gc > y0) median(r4, r3, r2, gc - 1);
+      if (CHAIN && gc > y0) median(r4, r3, r2, gc - 1);
       if (gc < gc_end) produce(r4, k);
     }
   };
@@ -943,19 +950,31 @@ __device__ __forceinline__ void m3_walk(M3Stream<FMT, R>& st, const unsigned cha
   const size_t frame_px = (size_t)g.W * g.H;
   unsigned gm[2], mm[2];
   column_masks(x, g.W, gm, mm);
-  if (f_begin == 0 && !st.hfirst) {
+  // First pass: gauss of the frame before the chunk's first output (forward)
+  // or of its last frame (backward, see motion_m3_kernel) into TMEM -- or
+  // the delay token.  A backward chunk's first gauss is the next delay token
+  // when it is the firing's last frame.
+  if (st.dir < 0 && f_end == g.frames) {
+    m3_pass<FMT, R, 3, INT>(st, nullptr, next_tok, next_copy, tmem, g, y0, x, lane, gm, mm);
+  } else if (st.dir > 0 && f_begin == 0 && !st.hfirst) {
     // Delay token: gauss of the previous firing's last frame -> TMEM.
     for (int r = 0; r < R + 2; ++r) {
       unsigned a0 = 0u, a1 = 0u;  // null token: black (proj/src/motion.cpp:131)
       if (prev_tok) load_bytes8<true>(prev_tok, y0 - 1 + r, x, g.W, g.H, a0, a1);
       tmem_st2(tmem + 2u * r, a0, a1);
     }
-  } else {  // gauss(f_begin - 1): the previous frame, or the inline halo frame
+  } else {  // gauss of the first frame read: f_begin - 1 (or the inline halo frame), or f_end - 1
     m3_pass<FMT, R, 0, INT>(st, nullptr, nullptr, nullptr, tmem, g, y0, x, lane, gm, mm);
   }
-  const int f_last = (f_end == g.frames) ? f_end - 1 : f_end;
-  for (int f = f_begin; f < f_last; ++f)
+  // Chain passes, ONE loop body for both directions (a second hot copy of the
+  // pass costs instruction-cache misses).  Backward: the pass on frame k - 1
+  // yields the output of frame k (|g(k) - g(k-1)| is symmetric).
+  const int f_last = (st.dir > 0 && f_end == g.frames) ? f_end - 1 : f_end;
+  const int n_chain = f_last - f_begin;
+  for (int j = 0; j < n_chain; ++j) {
+    const int f = st.dir > 0 ? f_begin + j : f_end - 1 - j;
     m3_pass<FMT, R, 1, INT>(st, out + (size_t)f * frame_px, nullptr, nullptr, tmem, g, y0, x, lane, gm, mm);
+  }
   if (f_last < f_end)
     m3_pass<FMT, R, 2, INT>(st, out + (size_t)f_last * frame_px, next_tok, next_copy, tmem, g, y0, x, lane, gm, mm);
 }
@@ -1016,9 +1035,20 @@ __global__ void __launch_bounds__(32 * kM3Warps, DF_M3_MINB) motion_m3_kernel(co
     next_copy = chan_write_wraps(io.delay_ch) ? io.delay_ch.storage : nullptr;
   }
   st.lane = lane;
-  const int f_first = (f_begin > 0 || st.hfirst) ? f_begin - 1 : f_begin;  // warm-up frame
+  // Odd chunks walk their frames backwards (DF_M3_ALT).  Every chunk but the
+  // first re-reads one frame its neighbour also reads -- the frame before
+  // it: forward chunk c+1's warm-up frame is forward chunk c's last frame,
+  // read at opposite ends of the walk, so the second read came from DRAM
+  // (~9 % extra input reads at 720p).  With alternating directions the two
+  // chunks sharing a boundary frame both read it FIRST (a backward chunk's
+  // warm-up and the next forward chunk's warm-up) or both LAST, at about
+  // the same time, and the second read hits L2.  Chunk 0 (delay token or
+  // inline halo) always walks forward.
+  const bool back = DF_M3_ALT && (chunk & 1) && f_begin < f_end;
+  st.dir = back ? -1 : 1;
+  const int f_first = back ? f_end - 1 : (f_begin > 0 || st.hfirst) ? f_begin - 1 : f_begin;  // first frame read
   st.fs = base + f_first;
-  const int passes = f_begin < f_end ? f_end - f_first : 0;
+  const int passes = f_begin >= f_end ? 0 : back ? f_end - f_begin + 1 : f_end - f_first;
   st.groups = (unsigned)passes * M3Stream<FMT, R>::GPP;
   if (lane == 0) {
     for (int s = 0; s < kM3Stages; ++s) mbar_init(st.bars + 8 * s, 1);
