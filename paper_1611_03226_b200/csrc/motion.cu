@@ -81,6 +81,7 @@ struct MotionGeom {
   unsigned wg[6];    // gray
   unsigned wh[8];    // horizontal gauss
   int l2hint;        // M3: L2 eviction hints on band-halo rows (large frames)
+  int m3_chunks, m3_bands;  // M3: warp task t -> chunk t % chunks, band (t / chunks) % bands, tile
 };
 
 
@@ -595,15 +596,22 @@ constexpr size_t kSmemBytes = sizeof(uint2) * kWarpsPerCta * (kBandRows + 2) * 3
 #ifndef DF_M3_RPS
 #define DF_M3_RPS 5
 #endif
+// DF_M3_WARPS: warps per CTA.  4 (default): 4 CTAs per SM, each allocating
+// 128 TMEM columns (one lane quarter per warp).  > 4: ONE CTA per SM that
+// allocates all 512 columns; warp w uses lane quarter w % 4 and column block
+// w / 4 (so R is capped by 2(R + 2) * ceil(WARPS / 4) <= 512).
+#ifndef DF_M3_WARPS
+#define DF_M3_WARPS 20
+#endif
 #ifndef DF_M3_ST
-#define DF_M3_ST 3
+#define DF_M3_ST (DF_M3_WARPS > 4 ? 2 : 3)
 #endif
 // Shared-memory row loads issued at the start of a step (before the
 // gauss/thres/median work) instead of right before their use: A/B
 // (profiles/r01_ab_motion_variants.txt) 4K R=59 -1.8 %, 720p R=54 +1.3 %
 // (ptxas allocates R=54 at the 128-register cap), so per band height.
 #ifndef DF_M3_MINB
-#define DF_M3_MINB 4  // __launch_bounds__ min blocks (register cap 65536 / (128 * MINB))
+#define DF_M3_MINB (DF_M3_WARPS > 4 ? 1 : 4)  // __launch_bounds__ min blocks (register cap 65536 / (32 * WARPS * MINB))
 #endif
 #ifndef DF_M3_EARLY_MIN_R
 #define DF_M3_EARLY_MIN_R 59
@@ -611,15 +619,19 @@ constexpr size_t kSmemBytes = sizeof(uint2) * kWarpsPerCta * (kBandRows + 2) * 3
 #ifndef DF_M3_ALT
 #define DF_M3_ALT 1  // odd temporal chunks walk backwards (shared boundary frames hit L2)
 #endif
-constexpr int kM3Warps = 4;
+constexpr int kM3Warps = DF_M3_WARPS;
 // Band heights R (template parameter): a frame pass fetches rows y0-3 ..
 // y0+R+2 (R + 6 rows, whole 5-row boxes), gauss(prev) holds R + 2 rows in
 // 2(R + 2) <= 128 TMEM columns.  launch_m3 picks R per frame geometry.
+constexpr int kTmemCols = kM3Warps > 4 ? 512 : 128;
 template <int R>
-constexpr bool m3_valid_r() { return (R + 6) % 5 == 0 && 2 * (R + 2) <= 128; }
+constexpr int m3_warp_cols() { return 2 * (R + 2); }
+template <int R>
+constexpr bool m3_valid_r() {
+  return (R + 6) % 5 == 0 && m3_warp_cols<R>() * ((kM3Warps + 3) / 4) <= kTmemCols;
+}
 constexpr int kM3RPS = DF_M3_RPS;
 constexpr int kM3Stages = DF_M3_ST;
-constexpr int kTmemCols = 128;
 static_assert(kM3RPS == 5, "one TMA box per 5-step iteration of the row loop (static in-box row offsets)");
 
 // A TMA box's innermost start must be 16-byte aligned, and a warp tile's
@@ -989,12 +1001,18 @@ __global__ void __launch_bounds__(32 * kM3Warps, DF_M3_MINB) motion_m3_kernel(co
   // addresses, ring addresses) as warp-uniform instead of emitting
   // per-unique-value loops around every tcgen05.ld/st.
   const int lane = threadIdx.x & 31, warp = __shfl_sync(0xffffffffu, (int)threadIdx.x >> 5, 0);
-  const int y0 = blockIdx.y * R;
-  const int tx0 = (int)blockIdx.x * kOutPxPerWarp - kPxPerLane;
+  // Warp task t (1-D grid): consecutive tasks are consecutive temporal chunks
+  // of one (tile, band), so a 4-warp CTA holds 4 chunks of one band as before.
+  const int task = (int)blockIdx.x * kM3Warps + warp;
+  const int chunk = task % g.m3_chunks;
+  const int band = (task / g.m3_chunks) % g.m3_bands;
+  const int tile = task / (g.m3_chunks * g.m3_bands);
+  const int y0 = band * R;
+  const int tx0 = tile * kOutPxPerWarp - kPxPerLane;
   const int x = tx0 + lane * kPxPerLane;
-  const int chunk = blockIdx.z * kM3Warps + warp;
   const int f_begin = chunk * g.chunk;
-  const int f_end = min(f_begin + g.chunk, g.frames);
+  // Tasks past the last tile (the grid's last CTA) walk no frames.
+  const int f_end = tx0 < g.W ? min(f_begin + g.chunk, g.frames) : f_begin;
 
   unsigned* tmem_slot = reinterpret_cast<unsigned*>(m3_smem + kM3Warps * m3_ring_bytes<FMT>() + kM3Warps * kM3Stages * 8);
   if (warp == 0) {
@@ -1057,7 +1075,10 @@ __global__ void __launch_bounds__(32 * kM3Warps, DF_M3_MINB) motion_m3_kernel(co
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const unsigned tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0) + ((unsigned)(32 * warp) << 16);
+  // Lane quarter warp % 4 (a warp may only access its own quarter), column
+  // block warp / 4.
+  const unsigned tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0) + ((unsigned)(32 * (warp & 3)) << 16) +
+                        (unsigned)((warp >> 2) * m3_warp_cols<R>());
 
   if (passes > 0) {
     if (lane == 0)
@@ -1239,7 +1260,13 @@ bool m3_eligible(const df_motion* m, const MotionIO& io, int frames) {
 // Band heights M3 is built for; launch_m3 picks the one whose grid fills
 // one wave best (cost model: waves x (frames per chunk + warm-up) x rows
 // fetched per pass).
+#if DF_M3_WARPS > 20
+constexpr int kM3Heights[3] = {29, 34, 39};  // 6 warps per lane quarter: 2(R + 2) <= 85 columns
+#elif DF_M3_WARPS > 16
+constexpr int kM3Heights[3] = {39, 44, 49};  // 5 warps per lane quarter: 2(R + 2) <= 102 columns
+#else
 constexpr int kM3Heights[3] = {49, 54, 59};
+#endif
 
 template <int FMT>
 const void* m3_kernel_fn(int ri) {
@@ -1260,14 +1287,15 @@ M3Plan m3_plan(const df_motion* m, int frames, int ri) {
   p.ri = ri;
   p.bands = (m->H + R - 1) / R;
   const int slots = std::max(1, m->m3_resident[ri] * m->sms);  // CTAs in one wave
-  const int per_slice = tiles * p.bands;
-  // Temporal chunks (one per warp, kM3Warps per CTA): as many CTA slices as
-  // fit ONE wave (a partial second wave would double the step time).
-  p.slices = std::max(1, slots / per_slice);
-  p.chunks = std::min(p.slices * kM3Warps, frames);
+  const int per_slice = tiles * p.bands;  // warp tasks per temporal chunk
+  // Temporal chunks (one warp task per (tile, band, chunk)): as many as fit
+  // ONE wave of warps (a partial second wave would double the step time).
+  p.slices = std::max(1, slots * kM3Warps / per_slice);
+  p.chunks = std::min(p.slices, frames);
+  if (kM3Warps == 4 && p.chunks > 4) p.chunks &= ~3;  // whole CTAs of one (tile, band)
   p.chunk = (frames + p.chunks - 1) / p.chunks;
   p.chunks = (frames + p.chunk - 1) / p.chunk;
-  const int ctas = per_slice * ((p.chunks + kM3Warps - 1) / kM3Warps);
+  const int ctas = (per_slice * p.chunks + kM3Warps - 1) / kM3Warps;
   const int waves = (ctas + slots - 1) / slots;
   p.cost = (double)waves * (p.chunk + (p.chunks > 1 ? 1 : 0)) * (R + 6);
   return p;
@@ -1286,6 +1314,8 @@ int launch_m3(df_motion* m, const MotionIO& io, int frames, cudaStream_t s) {
     if (ri >= 0 && ri < 3) best = m3_plan(m, frames, ri);
   }
   g.chunk = best.chunk;
+  g.m3_chunks = best.chunks;
+  g.m3_bands = best.bands;
   // Band-halo rows need the L2 hint only when a frame pass streams more than
   // L2 can hold between their two reads (4K: 24.9 MB RGB frames; not 720p).
   g.l2hint = (size_t)m->W * m->H * FMT >= (8u << 20) ? 1 : 0;
@@ -1317,7 +1347,7 @@ int launch_m3(df_motion* m, const MotionIO& io, int frames, cudaStream_t s) {
     DF_REQUIRE(cr == CUDA_SUCCESS, DF_ECUDA, "motion: cuTensorMapEncodeTiled (halo) failed (%d)", (int)cr);
   }
   const int tiles = (m->W + kOutPxPerWarp - 1) / kOutPxPerWarp;
-  dim3 grid(tiles, best.bands, (best.chunks + kM3Warps - 1) / kM3Warps);
+  dim3 grid((tiles * best.bands * best.chunks + kM3Warps - 1) / kM3Warps);
   if (getenv("DF_DEBUG"))
     fprintf(stderr, "motion_m3: R %d, resident %d/SM, grid %ux%ux%u, chunk %d frames, smem %zu\n",
             kM3Heights[best.ri], m->m3_resident[best.ri], grid.x, grid.y, grid.z, g.chunk, m3_smem_bytes<FMT>());
