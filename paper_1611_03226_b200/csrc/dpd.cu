@@ -577,6 +577,239 @@ __global__ void __launch_bounds__(THREADS, dpd_min_blocks<T>()) dpd_main_kernel(
   }
 }
 
+// ---------------------------------------------------------------------------
+// One-wave kernel for short fast-path grids (DPD-1: 16 blocks x 64 tiles =
+// 1024 CTAs).  The main kernel keeps each thread's window positions (x, |x|,
+// scale: 36 registers) live across the branch loop, which caps it at 5 CTAs
+// per SM -- 740 slots, so a 1024-tile grid runs a full wave and then a 38 %
+// wave at ~2 warps per SM sub-partition.  Here the raw window and |x| live in
+// shared memory and each branch rebuilds its poly window from them (scale_b
+// = the reference's repeated product from 1.0f, recomputed per position), so
+// the kernel fits DF_DPD_WAVE_MINB CTAs per SM and the whole grid is resident
+// at once.  Same arithmetic, same op order as dpd_main_kernel (bit-exact).
+// ---------------------------------------------------------------------------
+#ifndef DF_DPD_WAVE_MINB
+#define DF_DPD_WAVE_MINB 7
+#endif
+#ifndef DF_DPD_WAVE
+#define DF_DPD_WAVE 1
+#endif
+
+template <int T, int V, int THREADS, bool HALO>
+__global__ void __launch_bounds__(THREADS, DF_DPD_WAVE_MINB)
+    dpd_wave_kernel(DpdIO io, const float2* __restrict__ taps_g, unsigned period, unsigned* err,
+                    unsigned* done_counter, FastState fs) {
+  using C = MainCfg<T, V, THREADS>;
+  static_assert(C::WL, "warp-local windows");
+  constexpr int H1 = T - 1;
+  constexpr int HS = H1 > 0 ? H1 : 1;
+  constexpr int NW = THREADS / 32;
+  __shared__ float2 taps_s[kBranches * T];
+  __shared__ float2 xs_all[NW][C::W];  // raw window
+  __shared__ float mg_all[NW][C::W];   // |x| of the window
+  __shared__ float2 us_all[NW][C::WP];  // poly window of the current branch (then the output staging)
+  __shared__ float2 hist_s[kBranches * HS];
+  __shared__ int q_s[kBranches];
+
+  const unsigned long long p = blockIdx.x;  // block-major: block-start tiles dispatch first
+  const unsigned tile = blockIdx.y;
+  const uint32_t* ctrl = io_ctrl(io);
+  const float2* __restrict__ x = io_in(io);
+  float2* __restrict__ y = io_out(io);
+  const int tid = threadIdx.x, lt = tid & 31, warp = tid >> 5;
+  const int wb = warp * C::OW;
+  float2* xs = xs_all[warp];
+  float* mgs = mg_all[warp];
+  float2* u = us_all[warp];
+  const unsigned t0 = tile * C::S;
+  const int n = (int)min((unsigned)C::S, period - t0);
+  const size_t blk = (size_t)p * period;
+  constexpr int NTR = (kBranches * T + THREADS - 1) / THREADS;
+  float2 tr[NTR];
+#pragma unroll
+  for (int k = 0; k < NTR; ++k) {
+    const int i = tid + k * THREADS;
+    if (i < kBranches * T) tr[k] = __ldg(&taps_g[i]);
+  }
+  uint32_t mask = ctrl[p];
+  {
+    float xr[C::M], xi[C::M];
+#pragma unroll
+    for (int m = 0; m < C::M; ++m) {
+      const int w = lt + m * 32;
+      const long long s = (long long)t0 + wb - H1 + w;
+      float2 v = make_float2(0.f, 0.f);
+      if (w < C::W && wb + w < n + H1 && s >= 0) v = __ldg(&x[blk + s]);
+      xr[m] = v.x;
+      xi[m] = v.y;
+    }
+#pragma unroll
+    for (int k = 0; k < NTR; ++k) {
+      const int i = tid + k * THREADS;
+      if (i < kBranches * T) taps_s[i] = tr[k];
+    }
+    if (mask >> kBranches) {
+      if (tid == 0) atomicCAS(err, 0u, (unsigned)DF_ECONTROL);
+      mask &= (1u << kBranches) - 1;
+    }
+#pragma unroll
+    for (int m = 0; m < C::M; ++m) {
+      const int w = lt + m * 32;
+      if (m < C::M - 1 || w < C::W) {
+        xs[w] = make_float2(xr[m], xi[m]);
+        if (mask > 1u) mgs[w] = __fsqrt_rn(__fadd_rn(__fmul_rn(xr[m], xr[m]), __fmul_rn(xi[m], xi[m])));
+      }
+    }
+  }
+  float outr[V], outi[V];
+#pragma unroll
+  for (int j = 0; j < V; ++j) outr[j] = outi[j] = -0.0f;
+  if (tile == 0 && mask && H1 > 0) {
+    if (tid < 32) {
+      unsigned need = mask;
+      for (long long base = (long long)p; need && base > 0; base -= 32) {
+        const long long idx = base - 1 - tid;
+        const uint32_t m = idx >= 0 ? ctrl[idx] : 0u;
+        for (unsigned bits = need; bits; bits &= bits - 1) {
+          const int b = __ffs(bits);
+          const unsigned bal = __ballot_sync(0xffffffffu, (m >> (b - 1)) & 1u);
+          if (bal) {
+            if (tid == 0) q_s[b - 1] = (int)(base - __ffs(bal));
+            need &= ~(1u << (b - 1));
+          }
+        }
+      }
+      if (tid == 0)
+        for (unsigned bits = need; bits; bits &= bits - 1) q_s[__ffs(bits) - 1] = -1;
+      if (tid < kBranches && ((mask >> tid) & 1u)) atomicMax(&fs.last1[tid], (int)p + 1);
+    }
+    __syncthreads();
+    for (int it = tid; it < kBranches * H1; it += THREADS) {
+      const int bi = it / H1, j = it - bi * H1;
+      if (!((mask >> bi) & 1u)) continue;
+      const int q = q_s[bi];
+      if (q >= 0) {
+        const float2 v = __ldg(&x[(size_t)q * period + (period - 1 - j)]);
+        hist_s[it] = poly_sample(v.x, v.y, bi + 1);
+      } else {
+        hist_s[it] = carried_history<HALO>(fs, bi, j, H1);
+      }
+    }
+  }
+  __syncthreads();  // taps_s, hist_s
+  const int pt = pad_index(lt);
+  const bool has_hist = tile == 0 && tid < H1;
+  const int hslot = pad_index(H1 - 1 - (has_hist ? tid : 0));
+#pragma unroll 1
+  for (uint32_t bits = mask; bits; bits &= bits - 1) {
+    const int b = __ffs(bits);
+    // Poly window of branch b: scale_b = ((1*mag)*mag)... (b-1 products,
+    // dpd.cpp:69-71), recomputed per position from |x| in shared memory.
+#pragma unroll
+    for (int m = 0; m < C::M; ++m) {
+      const int w = lt + m * 32;
+      if (m < C::M - 1 || w < C::W) {
+        const float2 v = xs[w];
+        float2 o = v;  // b == 1: scale 1.0f, x * 1.0f == x exactly
+        if (b > 1) {
+          const float g = mgs[w];
+          float sc = g;
+#pragma unroll 1
+          for (int q = 2; q < b; ++q) sc = __fmul_rn(sc, g);
+          o = make_float2(__fmul_rn(v.x, sc), __fmul_rn(v.y, sc));
+        }
+        u[pt + m * 36] = o;
+      }
+    }
+    if (tile == 0) __syncwarp();
+    if (has_hist) u[hslot] = hist_s[(b - 1) * H1 + tid];
+    __syncwarp();
+    const float2* tb = taps_s + (b - 1) * T;
+    float ar[V], ai[V], wr[V], wi[V];
+    const int o0 = lt * V;
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      const float2 v = u[pad_index(o0 + H1 + j)];
+      wr[j] = v.x;
+      wi[j] = v.y;
+    }
+    {
+      const float2 t = tb[0];
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        ar[j] = __fsub_rn(__fmul_rn(t.x, wr[j]), __fmul_rn(t.y, wi[j]));
+        ai[j] = __fadd_rn(__fmul_rn(t.x, wi[j]), __fmul_rn(t.y, wr[j]));
+      }
+    }
+#pragma unroll
+    for (int k = 1; k < T; ++k) {
+#pragma unroll
+      for (int j = V - 1; j > 0; --j) {
+        wr[j] = wr[j - 1];
+        wi[j] = wi[j - 1];
+      }
+      const float2 v = u[pad_index(o0 + H1 - k)];
+      wr[0] = v.x;
+      wi[0] = v.y;
+      const float2 t = tb[k];
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        ar[j] = __fadd_rn(ar[j], __fsub_rn(__fmul_rn(t.x, wr[j]), __fmul_rn(t.y, wi[j])));
+        ai[j] = __fadd_rn(ai[j], __fadd_rn(__fmul_rn(t.x, wi[j]), __fmul_rn(t.y, wr[j])));
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      outr[j] = __fadd_rn(outr[j], ar[j]);
+      outi[j] = __fadd_rn(outi[j], ai[j]);
+    }
+    __syncwarp();  // the next branch (or the staging) rewrites u
+  }
+#pragma unroll
+  for (int j = 0; j < V; ++j)
+    u[pad_index(lt * V + j)] = make_float2(__fadd_rn(outr[j], 0.0f), __fadd_rn(outi[j], 0.0f));
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const int o = lt + 32 * i;
+    if (wb + o < n) y[blk + t0 + wb + o] = u[pad_index(o)];
+  }
+  // End of grid: as dpd_main_kernel (block-start tiles counted on plain
+  // firings, every CTA on channel firings).
+  const bool counted = io.channel_mode || tile == 0;
+  if (!counted) return;
+  __shared__ bool last;
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    const unsigned total = io.channel_mode ? gridDim.x * gridDim.y : gridDim.x;
+    last = atomicAdd(done_counter, 1u) == total - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int it = tid; it < kBranches * H1; it += THREADS) {
+    const int bi = it / H1, j = it - bi * H1;
+    const int q = *(volatile int*)&fs.last1[bi] - 1;
+    if (q >= 0) {
+      const float2 v = x[(size_t)q * period + (period - 1 - j)];
+      fs.state[bi * (kMaxTaps - 1) + j] = poly_sample(v.x, v.y, bi + 1);
+    } else if (HALO && fs.htail[bi]) {
+      fs.state[bi * (kMaxTaps - 1) + j] = carried_history<HALO>(fs, bi, j, H1);
+    }
+  }
+  __syncthreads();
+  if (tid < kBranches) fs.last1[tid] = 0;
+  if (tid == 0) {
+    *done_counter = 0;
+    if (io.channel_mode) {
+      chan_commit_read(io.ctrl_ch, io.ctrl_ch.rate);
+      chan_commit_read(io.in_ch, io.in_ch.rate);
+      chan_commit_write(io.out_ch, io.out_ch.rate);
+    }
+  }
+}
+
 // Generic-T fallback (T not 10/32): simple per-output loop, same op order.
 __global__ void dpd_main_generic_kernel(DpdIO io, const float2* __restrict__ taps_g,
                                         const float2* __restrict__ hist, unsigned period, int T,
@@ -687,6 +920,7 @@ struct df_dpd {
   float2* taps = nullptr;      // device, 10*T
   float2* state = nullptr;     // device, 10*(kMaxTaps-1): FirState per branch
   unsigned resident_ctas = 0;  // main-kernel CTAs resident on the device (prefetch distance)
+  unsigned resident_wave_ctas = 0;  // dpd_wave_kernel CTAs resident on the device (one wave)
   unsigned* scratch = nullptr; // [0] error word, [1] done counter, [4..13] fast-path last1
   float2* hist = nullptr;      // device history table, capacity hist_blocks
   int* act = nullptr;          // device active lists, 10*hist_blocks
@@ -750,7 +984,17 @@ int launch_dpd(df_dpd* d, const DpdIO& io, unsigned long long K, cudaStream_t s,
                                                 (int)d->T, err);
     DF_TRY(after_launch("dpd_prep_kernel"));
   }
-  if (d->T == 10 || d->T == 32) {
+  if (fast && d->T == 10 && DF_DPD_WAVE && d->resident_wave_ctas &&
+      K * ((d->period + kThreads * kV - 1) / (kThreads * kV)) <= d->resident_wave_ctas) {
+    // Short grid that fits one wave of dpd_wave_kernel (DPD-1).
+    const unsigned tiles = (d->period + kThreads * kV - 1) / (kThreads * kV);
+    const dim3 grid((unsigned)K, tiles);
+    if (htail)
+      dpd_wave_kernel<10, kV, kThreads, true><<<grid, kThreads, 0, s>>>(io, d->taps, d->period, err, done, fs);
+    else
+      dpd_wave_kernel<10, kV, kThreads, false><<<grid, kThreads, 0, s>>>(io, d->taps, d->period, err, done, fs);
+    DF_TRY(after_launch("dpd_wave_kernel"));
+  } else if (d->T == 10 || d->T == 32) {
     constexpr int S = kThreads * kV;
     const unsigned tiles = (d->period + S - 1) / S;
     DF_REQUIRE(K <= 65535u * 1024u, DF_EINVAL, "dpd: batch too large");
@@ -850,6 +1094,11 @@ int df_dpd_create(int device, uint32_t period, uint32_t T, const float* taps_hos
                                                                 kThreads, 0);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     d->resident_ctas = (unsigned)(per_sm * sms);
+    int per_sm_wave = 0;
+    if (e == cudaSuccess && T == 10)
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_wave, dpd_wave_kernel<10, kV, kThreads, false>,
+                                                        kThreads, 0);
+    d->resident_wave_ctas = (unsigned)(per_sm_wave * sms);
   }
   if (e != cudaSuccess) {
     int rc = cuda_status(e, "df_dpd_create");
