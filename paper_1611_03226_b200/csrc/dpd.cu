@@ -594,6 +594,9 @@ __global__ void __launch_bounds__(THREADS, dpd_min_blocks<T>()) dpd_main_kernel(
 #ifndef DF_DPD_WAVE
 #define DF_DPD_WAVE 1
 #endif
+#ifndef DF_DPD_WAVE_PDL
+#define DF_DPD_WAVE_PDL 1
+#endif
 
 template <int T, int V, int THREADS, bool HALO>
 __global__ void __launch_bounds__(THREADS, DF_DPD_WAVE_MINB)
@@ -613,10 +616,28 @@ __global__ void __launch_bounds__(THREADS, DF_DPD_WAVE_MINB)
 
   const unsigned long long p = blockIdx.x;  // block-major: block-start tiles dispatch first
   const unsigned tile = blockIdx.y;
+  const int tid = threadIdx.x, lt = tid & 31, warp = tid >> 5;
+#if DF_DPD_WAVE_PDL
+  // Programmatic dependent launch (one-wave grids only: a multi-wave grid's
+  // early dependents would sit in its later waves' slots).  The next firing
+  // may launch now and becomes resident as this grid's CTAs retire; it
+  // stages its taps (written by no kernel) and then waits for this whole
+  // grid -- and its memory -- before touching anything a firing produces.
+  asm volatile("griddepcontrol.launch_dependents;");
+#endif
+  constexpr int NTR0 = (kBranches * T + THREADS - 1) / THREADS;
+  float2 tr[NTR0];
+#pragma unroll
+  for (int k = 0; k < NTR0; ++k) {
+    const int i = tid + k * THREADS;
+    if (i < kBranches * T) tr[k] = __ldg(&taps_g[i]);
+  }
+#if DF_DPD_WAVE_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
   const uint32_t* ctrl = io_ctrl(io);
   const float2* __restrict__ x = io_in(io);
   float2* __restrict__ y = io_out(io);
-  const int tid = threadIdx.x, lt = tid & 31, warp = tid >> 5;
   const int wb = warp * C::OW;
   float2* xs = xs_all[warp];
   float* mgs = mg_all[warp];
@@ -624,13 +645,7 @@ __global__ void __launch_bounds__(THREADS, DF_DPD_WAVE_MINB)
   const unsigned t0 = tile * C::S;
   const int n = (int)min((unsigned)C::S, period - t0);
   const size_t blk = (size_t)p * period;
-  constexpr int NTR = (kBranches * T + THREADS - 1) / THREADS;
-  float2 tr[NTR];
-#pragma unroll
-  for (int k = 0; k < NTR; ++k) {
-    const int i = tid + k * THREADS;
-    if (i < kBranches * T) tr[k] = __ldg(&taps_g[i]);
-  }
+  constexpr int NTR = NTR0;
   uint32_t mask = ctrl[p];
   {
     float xr[C::M], xi[C::M];
@@ -988,11 +1003,19 @@ int launch_dpd(df_dpd* d, const DpdIO& io, unsigned long long K, cudaStream_t s,
       K * ((d->period + kThreads * kV - 1) / (kThreads * kV)) <= d->resident_wave_ctas) {
     // Short grid that fits one wave of dpd_wave_kernel (DPD-1).
     const unsigned tiles = (d->period + kThreads * kV - 1) / (kThreads * kV);
-    const dim3 grid((unsigned)K, tiles);
-    if (htail)
-      dpd_wave_kernel<10, kV, kThreads, true><<<grid, kThreads, 0, s>>>(io, d->taps, d->period, err, done, fs);
-    else
-      dpd_wave_kernel<10, kV, kThreads, false><<<grid, kThreads, 0, s>>>(io, d->taps, d->period, err, done, fs);
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3((unsigned)K, tiles);
+    lc.blockDim = dim3(kThreads);
+    lc.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = attr;
+    lc.numAttrs = DF_DPD_WAVE_PDL ? 1 : 0;
+    DF_CHECK_CUDA(htail ? cudaLaunchKernelEx(&lc, dpd_wave_kernel<10, kV, kThreads, true>, io, d->taps, d->period,
+                                             err, done, fs)
+                        : cudaLaunchKernelEx(&lc, dpd_wave_kernel<10, kV, kThreads, false>, io, d->taps, d->period,
+                                             err, done, fs));
     DF_TRY(after_launch("dpd_wave_kernel"));
   } else if (d->T == 10 || d->T == 32) {
     constexpr int S = kThreads * kV;
