@@ -597,6 +597,9 @@ __global__ void __launch_bounds__(THREADS, dpd_min_blocks<T>()) dpd_main_kernel(
 #ifndef DF_DPD_WAVE_PDL
 #define DF_DPD_WAVE_PDL 1
 #endif
+#ifndef DF_DPD_WAVE_L2PF
+#define DF_DPD_WAVE_L2PF 1
+#endif
 
 template <int T, int V, int THREADS, bool HALO>
 __global__ void __launch_bounds__(THREADS, DF_DPD_WAVE_MINB)
@@ -633,6 +636,20 @@ __global__ void __launch_bounds__(THREADS, DF_DPD_WAVE_MINB)
     if (i < kBranches * T) tr[k] = __ldg(&taps_g[i]);
   }
 #if DF_DPD_WAVE_PDL
+  // Raw-mode firings know their input address before the previous grid is
+  // done: warm L2 with this tile's window now (a prefetch only fills L2, the
+  // point of coherence, so a later write by the previous grid still wins;
+  // the loads proper come after the wait).  Channel firings resolve their
+  // region from device state the previous grid may still commit.
+  if (DF_DPD_WAVE_L2PF && !io.channel_mode && tid == 0) {
+    const long long s0 = (long long)blockIdx.y * C::S - (T - 1);
+    const long long a = (long long)blockIdx.x * period + (s0 > 0 ? s0 : 0);
+    const long long e = (long long)blockIdx.x * period + min((long long)period, (long long)(blockIdx.y + 1) * C::S);
+    const uintptr_t lo = reinterpret_cast<uintptr_t>(io.in + a) & ~(uintptr_t)15;
+    const uintptr_t hi = (reinterpret_cast<uintptr_t>(io.in + e) + 15) & ~(uintptr_t)15;
+    if (hi > lo)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"((unsigned)(hi - lo)) : "memory");
+  }
   asm volatile("griddepcontrol.wait;" ::: "memory");
 #endif
   const uint32_t* ctrl = io_ctrl(io);
