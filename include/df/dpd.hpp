@@ -12,6 +12,7 @@
 
 #include <complex>
 #include <cstdint>
+#include <istream>
 #include <span>
 #include <vector>
 
@@ -48,6 +49,15 @@ struct Params {
   std::span<const std::complex<float>> input;  // host, interleaved re/im
   std::span<std::complex<float>> output;
 };
+
+// The reference's text formats (dpd.hpp:112-120, dpd.cpp:393-462; the
+// parsers are in host/formats.cpp).  Schedule file: one entry per line, "k"
+// (branches 1..k) or "k: i1,i2,...,ik"; blank lines and '#' comments
+// skipped; k outside [2,10] rejected (std::runtime_error naming the line).
+// Taps file: one branch per line, taps_per_branch "re,im" pairs (10 in the
+// reference; up to 32 here); returned branch-major as Params::taps.
+std::vector<ConfigToken> parse_schedule(std::istream& in);
+std::vector<std::complex<float>> parse_taps(std::istream& in, unsigned taps_per_branch = 10);
 
 NetworkGraph build_network(const Params& params);
 std::uint64_t source_firings(const Params& params);  // launches

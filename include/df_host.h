@@ -85,6 +85,23 @@ int dfh_validate_demo(int which);  /* which: 0..6, see host_abi.cpp */
  * the producer's firing i before the consumer's firing i). */
 int dfh_delay_chain_run(int device, uint32_t token_rate, int sink_first, uint64_t firings, uint64_t* out_host);
 
+/* ---- data formats either side of the path (df/io.hpp, df/dpd.hpp) -------
+ * The reference's text and file formats (proj/src/dpd.cpp:393-462
+ * parse_schedule / parse_taps; proj/src/bench.cpp:25-97, :173-262 read_file
+ * / write_file / read_pgm and the raw-frame / cf32 inputs).  Status 8 =
+ * FormatError (the reference's ConfigError: unreadable, truncated or
+ * malformed file); parse errors are status 6 with the reference's message.
+ * Size queries: pass a NULL buffer to get the sizes, then call again. */
+int dfh_parse_schedule(const char* text, uint16_t* masks, size_t cap, size_t* count);
+int dfh_parse_taps(const char* text, uint32_t taps_per_branch, float* taps_out /* 10*T*2 floats */);
+int dfh_read_pgm(const char* path, uint8_t* pixels, size_t cap_bytes, unsigned* width, unsigned* height,
+                 uint64_t* frames);
+int dfh_write_pgm(const char* path, const uint8_t* pixels, uint64_t frames, unsigned width, unsigned height);
+int dfh_read_raw_frames(const char* path, unsigned width, unsigned height, int input_format, uint8_t* pixels,
+                        size_t cap_bytes, uint64_t* frames);
+int dfh_read_cf32(const char* path, float* samples_out, size_t cap_samples, uint64_t* samples);
+int dfh_write_file(const char* path, const void* data, size_t size);
+
 #ifdef __cplusplus
 }
 #endif

@@ -117,6 +117,9 @@ def ref():
         lib.ref_capacity_tokens.argtypes = [C.c_uint32, C.c_int]
         lib.ref_write_slot.argtypes = [C.c_uint32, C.c_int, C.c_uint]
         lib.ref_read_slot.argtypes = [C.c_uint32, C.c_int, C.c_uint]
+        lib.ref_parse_schedule.restype = C.c_long
+        lib.ref_parse_schedule.argtypes = [C.c_char_p, C.c_void_p, C.c_size_t]
+        lib.ref_parse_taps.argtypes = [C.c_char_p, C.c_void_p]
         lib.ref_mem_total.restype = C.c_uint64
         lib.ref_mem_total.argtypes = [C.c_int, C.c_uint, C.c_uint, C.c_uint32, C.c_uint32]
         _ref = lib

@@ -11,6 +11,7 @@
 #include <cstring>
 #include <exception>
 #include <span>
+#include <sstream>
 #include <string>
 #include <thread>
 #include <vector>
@@ -69,6 +70,35 @@ void ref_synth_frames(uint64_t frames, unsigned w, unsigned h, uint64_t seed, ui
 int ref_check_config(uint16_t mask) {
   try {
     dpd::check_config({mask});
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// The reference's own text parsers (dpd.cpp:393-462), for parity of
+// df::dpd::parse_schedule / parse_taps.  Returns the entry count, or -1.
+long ref_parse_schedule(const char* text, uint16_t* out, size_t cap) {
+  try {
+    std::istringstream in(text);
+    auto s = dpd::parse_schedule(in);
+    for (size_t i = 0; i < s.size() && i < cap; ++i) out[i] = s[i].active_mask;
+    return (long)s.size();
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+int ref_parse_taps(const char* text, float* out) {
+  try {
+    std::istringstream in(text);
+    auto t = dpd::parse_taps(in);
+    for (size_t b = 0; b < t.size(); ++b)
+      for (size_t k = 0; k < t[b].size(); ++k) {
+        out[2 * (b * t[b].size() + k)] = t[b][k].real();
+        out[2 * (b * t[b].size() + k) + 1] = t[b][k].imag();
+      }
     return 0;
   } catch (const std::exception& e) {
     g_err = e.what();

@@ -4,7 +4,10 @@
 #include <memory>
 #include <string>
 
+#include <sstream>
+
 #include "df/dpd.hpp"
+#include "df/io.hpp"
 #include "df/motion.hpp"
 #include "df/runtime.hpp"
 #include "df_cuda.h"
@@ -27,6 +30,9 @@ int guarded(F&& f) {
   } catch (const df::BuildError& e) {
     g_err = std::string("BuildError: ") + e.what();
     return 7;
+  } catch (const df::io::FormatError& e) {
+    g_err = std::string("FormatError: ") + e.what();
+    return 8;
   } catch (const df::ControlError& e) {
     g_err = std::string("ControlError: ") + e.what();
     return 5;
@@ -426,6 +432,82 @@ int dfh_validate_demo(int which) {
     build_network(actors, chans);
   });
   return rc == 0 ? n : -1;
+}
+
+
+int dfh_parse_schedule(const char* text, uint16_t* masks, size_t cap, size_t* count) {
+  return guarded([&] {
+    if (!text || !count) throw std::invalid_argument("dfh_parse_schedule: null argument");
+    std::istringstream in(text);
+    const auto sched = df::dpd::parse_schedule(in);
+    *count = sched.size();
+    if (masks) {
+      if (cap < sched.size()) throw std::invalid_argument("dfh_parse_schedule: buffer too small");
+      for (size_t i = 0; i < sched.size(); ++i) masks[i] = sched[i].active_mask;
+    }
+  });
+}
+
+int dfh_parse_taps(const char* text, uint32_t taps_per_branch, float* taps_out) {
+  return guarded([&] {
+    if (!text || !taps_out) throw std::invalid_argument("dfh_parse_taps: null argument");
+    std::istringstream in(text);
+    const auto taps = df::dpd::parse_taps(in, taps_per_branch);
+    std::memcpy(taps_out, taps.data(), taps.size() * sizeof(std::complex<float>));
+  });
+}
+
+int dfh_read_pgm(const char* path, uint8_t* pixels, size_t cap_bytes, unsigned* width, unsigned* height,
+                 uint64_t* frames) {
+  return guarded([&] {
+    if (!path || !width || !height || !frames) throw std::invalid_argument("dfh_read_pgm: null argument");
+    const auto s = df::io::read_pgm(path);
+    *width = s.width;
+    *height = s.height;
+    *frames = s.frames;
+    if (pixels) {
+      if (cap_bytes < s.pixels.size()) throw std::invalid_argument("dfh_read_pgm: buffer too small");
+      std::memcpy(pixels, s.pixels.data(), s.pixels.size());
+    }
+  });
+}
+
+int dfh_write_pgm(const char* path, const uint8_t* pixels, uint64_t frames, unsigned width, unsigned height) {
+  return guarded([&] {
+    if (!path || !pixels) throw std::invalid_argument("dfh_write_pgm: null argument");
+    df::io::write_pgm(path, pixels, frames, width, height);
+  });
+}
+
+int dfh_read_raw_frames(const char* path, unsigned width, unsigned height, int input_format, uint8_t* pixels,
+                        size_t cap_bytes, uint64_t* frames) {
+  return guarded([&] {
+    if (!path || !frames) throw std::invalid_argument("dfh_read_raw_frames: null argument");
+    const auto px = df::io::read_raw_frames(path, width, height, static_cast<unsigned>(input_format), frames);
+    if (pixels) {
+      if (cap_bytes < px.size()) throw std::invalid_argument("dfh_read_raw_frames: buffer too small");
+      std::memcpy(pixels, px.data(), px.size());
+    }
+  });
+}
+
+int dfh_read_cf32(const char* path, float* samples_out, size_t cap_samples, uint64_t* samples) {
+  return guarded([&] {
+    if (!path || !samples) throw std::invalid_argument("dfh_read_cf32: null argument");
+    const auto s = df::io::read_cf32(path);
+    *samples = s.size();
+    if (samples_out) {
+      if (cap_samples < s.size()) throw std::invalid_argument("dfh_read_cf32: buffer too small");
+      std::memcpy(samples_out, s.data(), s.size() * sizeof(std::complex<float>));
+    }
+  });
+}
+
+int dfh_write_file(const char* path, const void* data, size_t size) {
+  return guarded([&] {
+    if (!path || (!data && size)) throw std::invalid_argument("dfh_write_file: null argument");
+    df::io::write_file(path, data, size);
+  });
 }
 
 }  // extern "C"

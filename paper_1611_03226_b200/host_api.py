@@ -42,6 +42,15 @@ def lib():
         L.dfh_delay_chain_run.argtypes = [C.c_int, C.c_uint32, C.c_int, C.c_uint64, C.c_void_p]
         L.dfh_memory.argtypes = [C.c_int, C.c_uint, C.c_uint, C.c_uint32, C.c_uint32, C.c_int,
                                  C.POINTER(C.c_uint64)]
+        L.dfh_parse_schedule.argtypes = [C.c_char_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t)]
+        L.dfh_parse_taps.argtypes = [C.c_char_p, C.c_uint32, C.c_void_p]
+        L.dfh_read_pgm.argtypes = [C.c_char_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_uint), C.POINTER(C.c_uint),
+                                   C.POINTER(C.c_uint64)]
+        L.dfh_write_pgm.argtypes = [C.c_char_p, C.c_void_p, C.c_uint64, C.c_uint, C.c_uint]
+        L.dfh_read_raw_frames.argtypes = [C.c_char_p, C.c_uint, C.c_uint, C.c_int, C.c_void_p, C.c_size_t,
+                                          C.POINTER(C.c_uint64)]
+        L.dfh_read_cf32.argtypes = [C.c_char_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_uint64)]
+        L.dfh_write_file.argtypes = [C.c_char_p, C.c_void_p, C.c_size_t]
         _h = L
     return _h
 
@@ -156,3 +165,61 @@ def motion_run_resident(frames: np.ndarray, width: int, height: int, threshold: 
                                          n, width, height, threshold, rate, ctas, timeout_s, C.byref(ms),
                                          fir.ctypes.data_as(C.c_void_p)))
     return out, ms.value, dict(zip(MOTION_ACTORS, fir.tolist()))
+
+
+# ---- data formats (include/df_host.h, df/io.hpp; proj/src/bench.cpp, dpd.cpp:393-462) ----
+def parse_schedule(text: str) -> np.ndarray:
+    """The reference's schedule text format -> one 10-bit mask per entry (uint16)."""
+    n = C.c_size_t()
+    b = text.encode()
+    _check(lib().dfh_parse_schedule(b, None, 0, C.byref(n)))
+    out = np.empty(n.value, np.uint16)
+    _check(lib().dfh_parse_schedule(b, out.ctypes.data_as(C.c_void_p), out.size, C.byref(n)))
+    return out
+
+
+def parse_taps(text: str, taps_per_branch: int = 10) -> np.ndarray:
+    """The reference's taps text format -> (10, T, 2) float32 (branch-major re, im)."""
+    out = np.empty((10, taps_per_branch, 2), np.float32)
+    _check(lib().dfh_parse_taps(text.encode(), taps_per_branch, out.ctypes.data_as(C.c_void_p)))
+    return out
+
+
+def read_pgm(path: str):
+    """Concatenated binary PGM (P5) frames -> (pixels uint8 [frames, h, w], width, height)."""
+    w, h, f = C.c_uint(), C.c_uint(), C.c_uint64()
+    p = os.fsencode(path)
+    _check(lib().dfh_read_pgm(p, None, 0, C.byref(w), C.byref(h), C.byref(f)))
+    px = np.empty((f.value, h.value, w.value), np.uint8)
+    _check(lib().dfh_read_pgm(p, px.ctypes.data_as(C.c_void_p), px.nbytes, C.byref(w), C.byref(h), C.byref(f)))
+    return px, w.value, h.value
+
+
+def write_pgm(path: str, frames: np.ndarray, width: int, height: int):
+    frames = np.ascontiguousarray(frames, np.uint8)
+    n = frames.size // (width * height)
+    _check(lib().dfh_write_pgm(os.fsencode(path), frames.ctypes.data_as(C.c_void_p), n, width, height))
+
+
+def read_raw_frames(path: str, width: int, height: int, fmt: int = 1) -> np.ndarray:
+    f = C.c_uint64()
+    p = os.fsencode(path)
+    _check(lib().dfh_read_raw_frames(p, width, height, fmt, None, 0, C.byref(f)))
+    px = np.empty(f.value * width * height * fmt, np.uint8)
+    _check(lib().dfh_read_raw_frames(p, width, height, fmt, px.ctypes.data_as(C.c_void_p), px.nbytes, C.byref(f)))
+    return px
+
+
+def read_cf32(path: str) -> np.ndarray:
+    """Interleaved complex-f32 file -> float32 [2 * samples]."""
+    n = C.c_uint64()
+    p = os.fsencode(path)
+    _check(lib().dfh_read_cf32(p, None, 0, C.byref(n)))
+    out = np.empty(2 * n.value, np.float32)
+    _check(lib().dfh_read_cf32(p, out.ctypes.data_as(C.c_void_p), n.value, C.byref(n)))
+    return out
+
+
+def write_file(path: str, data: np.ndarray):
+    data = np.ascontiguousarray(data)
+    _check(lib().dfh_write_file(os.fsencode(path), data.ctypes.data_as(C.c_void_p), data.nbytes))
