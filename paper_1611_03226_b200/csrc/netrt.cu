@@ -467,6 +467,108 @@ __device__ void post_dpd_branch(const ActorDesc& A, const Frame& F) {
   if ((int)threadIdx.x < H1) state[threadIdx.x] = next[threadIdx.x];
 }
 
+// ---- motion actors, 4 px per thread (frames with W % 4 == 0) -------------
+// The same integer arithmetic as the fused motion kernel (motion.cu): the
+// horizontal [1 4 6 4 1] as IDP.4A dot products on packed bytes with a +8
+// bias per row sum (the vertical weights sum to 16, so the bias adds the
+// reference's +128 rounding, motion.cpp:45), the vertical pass on 16x2
+// packed lanes.  Ring slots are read with ld.global.cg (L2) as elsewhere;
+// each word's 15 (gauss) / 5 (median) loads are independent and issued
+// together (a variant sharing neighbour words through shuffles measured
+// 2-3x slower: tools/probe_resident_profile.py).
+__device__ __forceinline__ unsigned m_prmt(unsigned a, unsigned b, unsigned sel) {
+  unsigned d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
+}
+constexpr unsigned mW8(unsigned a, unsigned b, unsigned c, unsigned d) { return a | (b << 8) | (c << 16) | (d << 24); }
+
+// Gauss of the 4 px of word C (neighbour words L, R) in one row: 16x2 pairs.
+__device__ __forceinline__ void m_hgauss4(unsigned L, unsigned C, unsigned R, unsigned& p01, unsigned& p23) {
+  const unsigned h0 = __dp4a(L, mW8(0, 0, 1, 4), __dp4a(C, mW8(6, 4, 1, 0), 8u));
+  const unsigned h1 = __dp4a(L, mW8(0, 0, 0, 1), __dp4a(C, mW8(4, 6, 4, 1), 8u));
+  const unsigned h2 = __dp4a(C, mW8(1, 4, 6, 4), __dp4a(R, mW8(1, 0, 0, 0), 8u));
+  const unsigned h3 = __dp4a(C, mW8(0, 1, 4, 6), __dp4a(R, mW8(4, 1, 0, 0), 8u));
+  p01 = h1 * 65536u + h0;
+  p23 = h3 * 65536u + h2;
+}
+
+__device__ void fire_gauss4(const ActorDesc& A, const Frame& F, const Group& G, unsigned W, unsigned H) {
+  const unsigned Wq = W / 4;
+  const unsigned long long Sq = (unsigned long long)Wq * H, totalq = Sq * A.in[0].rate;
+  for (unsigned long long k = G.first(); k < totalq; k += G.step()) {
+    const unsigned long long f = k / Sq, idx = k % Sq;
+    const unsigned y = (unsigned)(idx / Wq), xq = (unsigned)(idx % Wq);
+    const unsigned* fr = reinterpret_cast<const unsigned*>(F.in_ptr[0]) + f * Sq;
+    const unsigned c = __ldcg(fr + idx);
+    unsigned v = c;  // rows y < 2 or >= H-2: gray copied (motion.cpp:34-37)
+    if (y >= 2 && y < H - 2) {
+      unsigned a0 = 0, a1 = 0;
+#pragma unroll
+      for (int dy = -2; dy <= 2; ++dy) {
+        const unsigned* row = fr + (unsigned long long)(y + dy) * Wq + xq;
+        const unsigned C = dy == 0 ? c : __ldcg(row);
+        const unsigned L = xq > 0 ? __ldcg(row - 1) : 0u, R = xq + 1 < Wq ? __ldcg(row + 1) : 0u;
+        unsigned p01, p23;
+        m_hgauss4(L, C, R, p01, p23);
+        const unsigned w = dy == 0 ? 6u : (dy == -1 || dy == 1) ? 4u : 1u;
+        a0 += w * p01;
+        a1 += w * p23;
+      }
+      v = m_prmt(a0, a1, 0x7531);  // (sum + 128) >> 8 per px: byte 1 of each 16-bit lane
+      // Columns x < 2 or x >= W-2: gray copied.
+      const unsigned x = 4 * xq;
+      if (x < 2) v = (v & 0xFFFF0000u) | (c & 0x0000FFFFu);
+      if (x + 4 > W - 2) v = (v & 0x0000FFFFu) | (c & 0xFFFF0000u);
+    }
+    for (unsigned o = 0; o < A.n_out; ++o) {
+      reinterpret_cast<unsigned*>(F.out_ptr[o])[k] = v;
+      // Fig. 2 phase-2 copy (slot 3r -> slot 0, channel.cpp:97-104) done by
+      // the writer of each word instead of the leader CTA afterwards.
+      const unsigned long long last = (unsigned long long)(A.out[o].rate - 1) * Sq;
+      if (((F.out_wrap >> o) & 1u) && k >= last) reinterpret_cast<unsigned*>(A.out[o].storage)[k - last] = v;
+    }
+  }
+}
+
+__device__ __forceinline__ void m_sort2(unsigned& p, unsigned& q) {
+  const unsigned t = __vminu4(p, q);
+  q = __vmaxu4(p, q);
+  p = t;
+}
+
+__device__ void fire_median4(const ActorDesc& A, const Frame& F, const Group& G, unsigned W, unsigned H) {
+  const unsigned Wq = W / 4;
+  const unsigned long long Sq = (unsigned long long)Wq * H, totalq = Sq * A.in[0].rate;
+  for (unsigned long long k = G.first(); k < totalq; k += G.step()) {
+    const unsigned long long f = k / Sq, idx = k % Sq;
+    const unsigned y = (unsigned)(idx / Wq), xq = (unsigned)(idx % Wq);
+    const unsigned* fr = reinterpret_cast<const unsigned*>(F.in_ptr[0]) + f * Sq;
+    const unsigned c = __ldcg(fr + idx);
+    unsigned v = c;  // rows 0 and H-1: copied (motion.cpp:64-67)
+    if (y >= 1 && y < H - 1) {
+      unsigned a = c, b = __ldcg(fr + idx - Wq), cc = __ldcg(fr + idx + Wq);
+      const unsigned lw = xq > 0 ? __ldcg(fr + idx - 1) : 0u, rw = xq + 1 < Wq ? __ldcg(fr + idx + 1) : 0u;
+      unsigned d = __funnelshift_l(lw, c, 8), e = __funnelshift_r(c, rw, 8);  // left / right neighbours
+      // median of 5 per byte: the scalar actor's sorting network on 4 lanes
+      m_sort2(a, b); m_sort2(d, e); m_sort2(a, cc); m_sort2(b, cc); m_sort2(a, d);
+      m_sort2(cc, d); m_sort2(b, e); m_sort2(b, cc); m_sort2(d, e);
+      v = cc;
+      const unsigned x = 4 * xq;
+      if (x == 0) v = (v & 0xFFFFFF00u) | (c & 0xFFu);              // column 0 copied
+      if (x + 4 == W) v = (v & 0x00FFFFFFu) | (c & 0xFF000000u);    // column W-1 copied
+    }
+    reinterpret_cast<unsigned*>(F.out_ptr[0])[k] = v;
+  }
+}
+
+__device__ __forceinline__ bool words_ok(const Frame& F, const ActorDesc& A, unsigned W) {
+  uintptr_t m = W & 3u;
+  for (unsigned p = 0; p < A.n_in; ++p) m |= reinterpret_cast<uintptr_t>(F.in_ptr[p]);
+  for (unsigned p = 0; p < A.n_out; ++p) m |= reinterpret_cast<uintptr_t>(F.out_ptr[p]);
+  return (m & 3u) == 0;
+}
+
 __device__ void fire_kind(const ActorDesc& A, const Frame& F, const Group& G, ActorRt* rt, float2* win) {
   switch (A.kind) {
     case DF_ACT_DPD_SOURCE: {  // dpd.cpp:189-204
@@ -577,6 +679,10 @@ __device__ void fire_kind(const ActorDesc& A, const Frame& F, const Group& G, Ac
     case DF_ACT_GAUSS: {  // gauss5x5 (motion.cpp:27-48) of every frame, to every output
       const df_act_frames& P = params<df_act_frames>(A);
       const unsigned W = P.width, H = P.height;
+      if (W >= 8 && H >= 5 && words_ok(F, A, W)) {
+        fire_gauss4(A, F, G, W, H);
+        break;
+      }
       const unsigned long long S = (unsigned long long)W * H, total = S * A.in[0].rate;
       const unsigned char* in = F.in_ptr[0];
       for (unsigned long long k = G.first(); k < total; k += G.step()) {
@@ -594,7 +700,11 @@ __device__ void fire_kind(const ActorDesc& A, const Frame& F, const Group& G, Ac
               acc += bn[dy + 2] * bn[dx + 2] * (int)__ldcg(fr + (unsigned long long)(y + dy) * W + (x + dx));
           v = (unsigned)((acc + 128) >> 8);
         }
-        for (unsigned o = 0; o < A.n_out; ++o) F.out_ptr[o][k] = (unsigned char)v;
+        for (unsigned o = 0; o < A.n_out; ++o) {
+          F.out_ptr[o][k] = (unsigned char)v;
+          const unsigned long long last = (unsigned long long)(A.out[o].rate - 1) * S;  // phase-2 copy inline
+          if (((F.out_wrap >> o) & 1u) && k >= last) A.out[o].storage[k - last] = (unsigned char)v;
+        }
       }
       break;
     }
@@ -621,6 +731,10 @@ __device__ void fire_kind(const ActorDesc& A, const Frame& F, const Group& G, Ac
     case DF_ACT_MEDIAN: {  // median5 (motion.cpp:59-74): plus-shaped median, 1-px border copy
       const df_act_frames& P = params<df_act_frames>(A);
       const unsigned W = P.width, H = P.height;
+      if (W >= 8 && H >= 3 && words_ok(F, A, W)) {
+        fire_median4(A, F, G, W, H);
+        break;
+      }
       const unsigned long long S = (unsigned long long)W * H, total = S * A.in[0].rate;
       for (unsigned long long k = G.first(); k < total; k += G.step()) {
         const unsigned long long f = k / S, idx = k % S;
@@ -772,7 +886,7 @@ __global__ void __launch_bounds__(kNetThreads, 4) net_kernel(const ActorDesc* __
     post_kind(A, s_frame, rt);
     // Fig. 2 phase-2 write: copy slot 3r into slot 0 (channel.cpp:97-104).
     for (unsigned p = 0; p < A.n_out; ++p)
-      if ((s_frame.out_wrap >> p) & 1u) {
+      if (((s_frame.out_wrap >> p) & 1u) && A.kind != DF_ACT_GAUSS) {  // GAUSS writes it inline
         const DevChan& c = A.out[p];
         copy_bytes(c.storage, c.storage + 3ull * c.rate * c.token_size, c.token_size, Group{0, 1});
       }

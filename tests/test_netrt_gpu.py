@@ -116,6 +116,16 @@ def test_resident_motion_fixture_64x48(gpu, small):
     assert fir == {"source": 16, "gauss": 16, "thres": 16, "med": 16, "sink": 16}
 
 
+@pytest.mark.parametrize("w,h", [(40, 9), (8, 5), (37, 23), (1280, 72)])
+def test_resident_motion_sizes_vs_oracle(gpu, w, h):
+    # Word-wise gauss/median actors (W % 4 == 0: 40x9, 8x5 at the 5-row /
+    # 8-column minimum, 1280x72) and the byte-wise fallback (37x23).
+    from paper_1611_03226_b200 import host_api as H
+    f = O.synth_bytes(6 * w * h, 7000 + w)
+    out, _, _ = H.motion_run_resident(f, w, h, 32, ctas=4)
+    np.testing.assert_array_equal(out, O.motion_gray(f, w, h, 32))
+
+
 @pytest.mark.parametrize("rate", [1, 4])
 def test_resident_motion_acceptance6(gpu, hashes, rate):
     # acceptance.cpp:328-341 at r = 1 and 4: at r = 4 the thres actor's prev
