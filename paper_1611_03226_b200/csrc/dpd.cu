@@ -597,6 +597,9 @@ __global__ void __launch_bounds__(THREADS, dpd_min_blocks<T>()) dpd_main_kernel(
 #ifndef DF_DPD_WAVE_PDL
 #define DF_DPD_WAVE_PDL 1
 #endif
+#ifndef DF_DPD_WAVE_ALL
+#define DF_DPD_WAVE_ALL 0  // A/B: the shared-memory-window kernel for every T=10 fast-path grid
+#endif
 #ifndef DF_DPD_WAVE_L2PF
 #define DF_DPD_WAVE_L2PF 1
 #endif
@@ -1016,8 +1019,10 @@ int launch_dpd(df_dpd* d, const DpdIO& io, unsigned long long K, cudaStream_t s,
                                                 (int)d->T, err);
     DF_TRY(after_launch("dpd_prep_kernel"));
   }
-  if (fast && d->T == 10 && DF_DPD_WAVE && d->resident_wave_ctas &&
-      K * ((d->period + kThreads * kV - 1) / (kThreads * kV)) <= d->resident_wave_ctas) {
+  const bool one_wave = d->resident_wave_ctas &&
+                        K * ((d->period + kThreads * kV - 1) / (kThreads * kV)) <= d->resident_wave_ctas;
+  if (fast && d->T == 10 && DF_DPD_WAVE && d->resident_wave_ctas && (one_wave || DF_DPD_WAVE_ALL) &&
+      K <= 65535) {
     // Short grid that fits one wave of dpd_wave_kernel (DPD-1).
     const unsigned tiles = (d->period + kThreads * kV - 1) / (kThreads * kV);
     cudaLaunchConfig_t lc{};
@@ -1028,7 +1033,7 @@ int launch_dpd(df_dpd* d, const DpdIO& io, unsigned long long K, cudaStream_t s,
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     lc.attrs = attr;
-    lc.numAttrs = DF_DPD_WAVE_PDL ? 1 : 0;
+    lc.numAttrs = DF_DPD_WAVE_PDL && one_wave ? 1 : 0;
     DF_CHECK_CUDA(htail ? cudaLaunchKernelEx(&lc, dpd_wave_kernel<10, kV, kThreads, true>, io, d->taps, d->period,
                                              err, done, fs)
                         : cudaLaunchKernelEx(&lc, dpd_wave_kernel<10, kV, kThreads, false>, io, d->taps, d->period,
