@@ -804,13 +804,13 @@ def resident_networks():
     from paper_1611_03226_b200 import host_api as H
     x = O.synth_samples(1 << 20, 810)
     taps = O.random_taps(808)
-    H.dpd_run_resident(x, taps, [3], 65536)
-    ms = [H.dpd_run_resident(x, taps, [3], 65536)[1] for _ in range(3)]
+    H.dpd_run_resident(x, taps, [3], 65536, branch_ctas=32)
+    ms = [H.dpd_run_resident(x, taps, [3], 65536, branch_ctas=32)[1] for _ in range(3)]
     f = O.synth_bytes(300 * 1280 * 720, 5)
     mm = [H.motion_run_resident(f, 1280, 720, 32, ctas=96)[1] for _ in range(2)]
     return {"dpd1": {"value": round((1 << 20) / (statistics.median(ms) / 1e3) / 1e6, 1), "unit": "Msamples/s",
                      "path": "dfh_dpd_run_resident: source, config, split, 10 branches, adder, sink (56 channels), "
-                             "16 CTAs per branch"},
+                             "32 CTAs per branch"},
             "motion720gray": {"value": round(300 / (statistics.median(mm) / 1e3), 1), "unit": "frames/s",
                               "path": "dfh_motion_run_resident: source, gauss, thres, med, sink with the "
                                       "gauss_thres_prev delay channel, 96 CTAs per actor"},

@@ -44,6 +44,7 @@ namespace df {
 namespace {
 
 constexpr int kMaxPorts = 24;
+constexpr unsigned kMaxPairs = 10;  // DPD adder: up to 10 (re, im) input pairs
 constexpr int kNetThreads = 256;
 constexpr int kParamBytes = 96;
 
@@ -397,6 +398,9 @@ __device__ __noinline__ void copy_bytes(unsigned char* dst, const unsigned char*
   }
 }
 
+// The branch actor's window: kBranchV consecutive outputs per thread.
+constexpr int kBranchV = 4;
+
 __device__ void fire_dpd_branch(const ActorDesc& A, const Frame& F, const Group& G, float2* win) {
   const df_act_branch& P = params<df_act_branch>(A);
   if (!(F.in_on & 1u)) return;  // inactive this period: no I/O, state frozen (dpd.cpp:272)
@@ -408,41 +412,82 @@ __device__ void fire_dpd_branch(const ActorDesc& A, const Frame& F, const Group&
   const float2* state = reinterpret_cast<const float2*>(P.state);
   const int T = (int)P.taps_per_branch, H1 = T - 1, b = (int)P.branch;
   const unsigned n = P.period;
-  // Chunks of blockDim outputs, round-robin over the group's CTAs; the poly
-  // window (chunk + T-1 history) is staged in shared memory.  The raw
-  // inputs of a thread's window positions (w = tid, tid + blockDim) are
-  // loaded one chunk ahead, so each chunk's FIR hides the next loads.
-  const unsigned stride = G.ctas * blockDim.x;
+  // Chunks of C = kBranchV * blockDim outputs, round-robin over the group's
+  // CTAs; the poly window (chunk + T-1 history) is staged in shared memory
+  // and each thread runs a register-blocked FIR over kBranchV consecutive
+  // outputs (a sliding window over the taps: kBranchV independent
+  // accumulation chains per component).  The raw inputs of the next chunk
+  // are loaded before this chunk's FIR.
+  constexpr int V = kBranchV;
+  const unsigned C = V * blockDim.x;
+  const unsigned stride = G.ctas * C;
+  constexpr int MW = V + 1;  // window positions per thread: C + T-1 <= (V+1) * blockDim for T <= 33
   auto raw = [&](unsigned c0, int w) -> float2 {
     const long long j = (long long)c0 - H1 + w;
-    if (w >= (int)blockDim.x + H1 || j >= (long long)n) return make_float2(0.f, 0.f);
+    if (w >= (int)C + H1 || j >= (long long)n) return make_float2(0.f, 0.f);
     if (j >= 0) return make_float2(__ldcg(re + j), __ldcg(im + j));
     return __ldcg(state - j - 1);  // FirState x[-(j+1)] (fir10, dpd.cpp:92-97), written by the leader CTA
   };
-  float2 nx0 = raw(G.g * blockDim.x, threadIdx.x), nx1 = raw(G.g * blockDim.x, threadIdx.x + blockDim.x);
-  for (unsigned c0 = G.g * blockDim.x; c0 < n; c0 += stride) {
-    const float2 x0 = nx0, x1 = nx1;
+  float2 nx[MW];
+#pragma unroll
+  for (int m = 0; m < MW; ++m) nx[m] = raw(G.g * C, threadIdx.x + m * blockDim.x);
+  for (unsigned c0 = G.g * C; c0 < n; c0 += stride) {
+    float2 x[MW];
+#pragma unroll
+    for (int m = 0; m < MW; ++m) x[m] = nx[m];
     if (c0 + stride < n) {
-      nx0 = raw(c0 + stride, threadIdx.x);
-      nx1 = raw(c0 + stride, threadIdx.x + blockDim.x);
+#pragma unroll
+      for (int m = 0; m < MW; ++m) nx[m] = raw(c0 + stride, threadIdx.x + m * blockDim.x);
     }
-    __syncthreads();
+    __syncthreads();  // the previous chunk's FIR has read the window
     // poly of the raw samples; history positions before the block start are
     // already poly outputs (the FirState).
-    const long long j0 = (long long)c0 - H1 + threadIdx.x, j1 = j0 + blockDim.x;
-    win[threadIdx.x] = j0 >= 0 ? poly_sample(x0.x, x0.y, b) : x0;
-    if ((int)threadIdx.x < H1) win[threadIdx.x + blockDim.x] = j1 >= 0 ? poly_sample(x1.x, x1.y, b) : x1;
-    __syncthreads();
-    const unsigned o = c0 + threadIdx.x;
-    if (o < n) {
-      float ar = 0.0f, ai = 0.0f;  // fir10's accumulation order (dpd.cpp:87-104)
-      for (int k = 0; k < T; ++k) {
-        const float2 t = taps[k], x = win[threadIdx.x + H1 - k];
-        ar = __fadd_rn(ar, __fsub_rn(__fmul_rn(t.x, x.x), __fmul_rn(t.y, x.y)));
-        ai = __fadd_rn(ai, __fadd_rn(__fmul_rn(t.x, x.y), __fmul_rn(t.y, x.x)));
+#pragma unroll
+    for (int m = 0; m < MW; ++m) {
+      const int w = threadIdx.x + m * blockDim.x;
+      if (w < (int)C + H1) {
+        const long long j = (long long)c0 - H1 + w;
+        win[w] = j >= 0 ? poly_sample(x[m].x, x[m].y, b) : x[m];
       }
-      ore[o] = ar;
-      oim[o] = ai;
+    }
+    __syncthreads();
+    const unsigned o0 = c0 + V * threadIdx.x;
+    if (o0 < n) {
+      // fir10's accumulation order per output (dpd.cpp:87-104): 0.0f, then
+      // taps k ascending.  Output o0 + j reads window index V*tid + j + H1 - k.
+      float ar[V], ai[V], wr[V], wi[V];
+      const int base = V * threadIdx.x + H1;
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        const float2 v = win[base + j];
+        wr[j] = v.x;
+        wi[j] = v.y;
+        ar[j] = ai[j] = 0.0f;
+      }
+      for (int k = 0; k < T; ++k) {
+        if (k > 0) {
+#pragma unroll
+          for (int j = V - 1; j > 0; --j) {
+            wr[j] = wr[j - 1];
+            wi[j] = wi[j - 1];
+          }
+          const float2 v = win[base - k];
+          wr[0] = v.x;
+          wi[0] = v.y;
+        }
+        const float2 t = taps[k];
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          ar[j] = __fadd_rn(ar[j], __fsub_rn(__fmul_rn(t.x, wr[j]), __fmul_rn(t.y, wi[j])));
+          ai[j] = __fadd_rn(ai[j], __fadd_rn(__fmul_rn(t.x, wi[j]), __fmul_rn(t.y, wr[j])));
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < V; ++j)
+        if (o0 + j < n) {
+          ore[o0 + j] = ar[j];
+          oim[o0 + j] = ai[j];
+        }
     }
   }
 }
@@ -619,8 +664,10 @@ __device__ void fire_kind(const ActorDesc& A, const Frame& F, const Group& G, Ac
         const unsigned long long s1 = s0 + G.step();
         const bool two = s1 < n;
         float r0 = 0.0f, i0 = 0.0f, r1 = 0.0f, i1 = 0.0f;
-#pragma unroll 1
-        for (unsigned p = 0; p + 1 < A.n_in; p += 2) {
+        // Unrolled over the (at most 10) input pairs so every active input's
+        // loads are issued before the adds consume them.
+#pragma unroll
+        for (unsigned p = 0; p + 1 < 2 * kMaxPairs && p + 1 < A.n_in; p += 2) {
           if (!((F.in_on >> p) & 1u)) continue;
           const float* pr = reinterpret_cast<const float*>(F.in_ptr[p]);
           const float* pi = reinterpret_cast<const float*>(F.in_ptr[p + 1]);
@@ -802,7 +849,7 @@ __global__ void __launch_bounds__(kNetThreads, 4) net_kernel(const ActorDesc* __
                                                           ActorRt* rts, NetCtl* ctl) {
   __shared__ int s_actor;
   __shared__ Frame s_frame;
-  __shared__ float2 win[kNetThreads + 32];
+  __shared__ float2 win[kBranchV * kNetThreads + 32];  // DPD branch window (chunk + T-1 history)
   __shared__ bool s_aborted;
   __shared__ Phases s_ph;  // leader CTA: the actor's endpoint phases
   __shared__ unsigned long long s_t;  // leader: timestamp of the current phase
