@@ -281,6 +281,82 @@ __device__ __forceinline__ float2 carried_history(const FastState& fs, int bi, i
   return fs.state[bi * (kMaxTaps - 1) + j];
 }
 
+// Block-start tile of block p (fast path): resolve every active branch's
+// FIR history into hist_s[b * H1 + j] = u_b[-(j+1)].  Warp 0 scans the
+// control tokens back from p, 32 per step (lowest set lane = most recent
+// block), for each branch's last earlier active block q; the history is
+// poly of q's last T-1 inputs, or the carried FirState / halo when the
+// branch has no earlier active block.  Also publishes p into last1 for the
+// end-of-grid FirState hand-off.  CTA-collective (two __syncthreads).
+template <bool HALO, int NT>
+__device__ __forceinline__ void dpd_block_history(const uint32_t* ctrl, const float2* __restrict__ x,
+                                                  unsigned long long p, uint32_t mask, unsigned period, int H1,
+                                                  const FastState& fs, int* q_s, float2* hist_s, int tid) {
+  if (tid < 32) {
+    unsigned need = mask;
+    for (long long base = (long long)p; need && base > 0; base -= 32) {
+      const long long idx = base - 1 - tid;
+      const uint32_t m = idx >= 0 ? ctrl[idx] : 0u;
+      for (unsigned bits = need; bits; bits &= bits - 1) {
+        const int b = __ffs(bits);
+        const unsigned bal = __ballot_sync(0xffffffffu, (m >> (b - 1)) & 1u);
+        if (bal) {
+          if (tid == 0) q_s[b - 1] = (int)(base - __ffs(bal));
+          need &= ~(1u << (b - 1));
+        }
+      }
+    }
+    if (tid == 0)
+      for (unsigned bits = need; bits; bits &= bits - 1) q_s[__ffs(bits) - 1] = -1;
+    if (tid < kBranches && ((mask >> tid) & 1u)) atomicMax(&fs.last1[tid], (int)p + 1);
+  }
+  __syncthreads();
+  for (int it = tid; it < kBranches * H1; it += NT) {
+    const int bi = it / H1, j = it - bi * H1;
+    if (!((mask >> bi) & 1u)) continue;
+    const int q = q_s[bi];
+    if (q >= 0) {
+      const float2 v = __ldg(&x[(size_t)q * period + (period - 1 - j)]);
+      hist_s[it] = poly_sample(v.x, v.y, bi + 1);
+    } else {
+      hist_s[it] = carried_history<HALO>(fs, bi, j, H1);
+    }
+  }
+  __syncthreads();
+}
+
+// End of a firing, run by the last counted CTA: advance the carried FirState
+// to the tails of each branch's last active block of the batch (every
+// block-start tile has read the old state by now; a branch gated off all
+// batch keeps its state, or takes the halo tail), reset the batch words and
+// commit a channel firing (K control tokens, K blocks in, K blocks out).
+template <bool HALO, int NT>
+__device__ __forceinline__ void dpd_grid_end(const DpdIO& io, const float2* x, unsigned period, int H1, bool fast,
+                                             const FastState& fs, unsigned* done_counter, int tid) {
+  if (fast) {
+    for (int it = tid; it < kBranches * H1; it += NT) {
+      const int bi = it / H1, j = it - bi * H1;
+      const int q = *(volatile int*)&fs.last1[bi] - 1;
+      if (q >= 0) {
+        const float2 v = x[(size_t)q * period + (period - 1 - j)];
+        fs.state[bi * (kMaxTaps - 1) + j] = poly_sample(v.x, v.y, bi + 1);
+      } else if (HALO && fs.htail[bi]) {  // gated off all batch: the halo becomes the state
+        fs.state[bi * (kMaxTaps - 1) + j] = carried_history<HALO>(fs, bi, j, H1);
+      }
+    }
+    __syncthreads();
+    if (tid < kBranches) fs.last1[tid] = 0;
+  }
+  if (tid == 0) {
+    *done_counter = 0;
+    if (io.channel_mode) {
+      chan_commit_read(io.ctrl_ch, io.ctrl_ch.rate);
+      chan_commit_read(io.in_ch, io.in_ch.rate);
+      chan_commit_write(io.out_ch, io.out_ch.rate);
+    }
+  }
+}
+
 // HALO: the firing takes per-branch halo tails (df_dpd_fire_halo); a
 // separate instantiation, so plain firings keep their register allocation
 // (with the tails compiled in, DPD-1 ran 7 % slower).
@@ -377,43 +453,8 @@ __global__ void __launch_bounds__(THREADS, dpd_min_blocks<T>()) dpd_main_kernel(
 #pragma unroll
   for (int j = 0; j < V; ++j) outr[j] = outi[j] = -0.0f;
   constexpr bool fast = FAST;
-  if (fast && tile == 0 && mask && H1 > 0) {
-    // Last earlier active block per active branch: warp 0 scans the tokens
-    // back from p, 32 per step (lowest set lane = most recent block).
-    if (tid < 32) {
-      unsigned need = mask;
-      for (long long base = (long long)p; need && base > 0; base -= 32) {
-        const long long idx = base - 1 - tid;
-        const uint32_t m = idx >= 0 ? ctrl[idx] : 0u;
-        for (unsigned bits = need; bits; bits &= bits - 1) {
-          const int b = __ffs(bits);
-          const unsigned bal = __ballot_sync(0xffffffffu, (m >> (b - 1)) & 1u);
-          if (bal) {
-            if (tid == 0) q_s[b - 1] = (int)(base - __ffs(bal));
-            need &= ~(1u << (b - 1));
-          }
-        }
-      }
-      if (tid == 0)
-        for (unsigned bits = need; bits; bits &= bits - 1) q_s[__ffs(bits) - 1] = -1;
-      if (tid < kBranches && ((mask >> tid) & 1u)) atomicMax(&fs.last1[tid], (int)p + 1);
-    }
-    __syncthreads();
-    // hist_s[b][j] = u_b[-(j+1)]: poly of block q's sample period-1-j, or
-    // the carried FirState[j] when the branch has no earlier active block.
-    for (int it = tid; it < kBranches * H1; it += THREADS) {
-      const int bi = it / H1, j = it - bi * H1;
-      if (!((mask >> bi) & 1u)) continue;
-      const int q = q_s[bi];
-      if (q >= 0) {
-        const float2 v = __ldg(&x[(size_t)q * period + (period - 1 - j)]);
-        hist_s[it] = poly_sample(v.x, v.y, bi + 1);
-      } else {
-        hist_s[it] = carried_history<HALO>(fs, bi, j, H1);
-      }
-    }
-    __syncthreads();
-  }
+  if (fast && tile == 0 && mask && H1 > 0)
+    dpd_block_history<HALO, THREADS>(ctrl, x, p, mask, period, H1, fs, q_s, hist_s, tid);
   if (!fast && tile == 0) asm volatile("griddepcontrol.wait;" ::: "memory");  // history table from prep
   if (C::WL) __syncthreads();  // taps_s (and hist_s) before the first branch
   int prev_b = 1;
@@ -552,28 +593,7 @@ __global__ void __launch_bounds__(THREADS, dpd_min_blocks<T>()) dpd_main_kernel(
     __syncthreads();
     if (!last) return;
     __threadfence();
-    if (fast) {
-      for (int it = tid; it < kBranches * H1; it += THREADS) {
-        const int bi = it / H1, j = it - bi * H1;
-        const int q = *(volatile int*)&fs.last1[bi] - 1;
-        if (q >= 0) {
-          const float2 v = x[(size_t)q * period + (period - 1 - j)];
-          fs.state[bi * (kMaxTaps - 1) + j] = poly_sample(v.x, v.y, bi + 1);
-        } else if (HALO && fs.htail[bi]) {  // gated off all batch: the halo becomes the state
-          fs.state[bi * (kMaxTaps - 1) + j] = carried_history<HALO>(fs, bi, j, H1);
-        }
-      }
-      __syncthreads();
-      if (tid < kBranches) fs.last1[tid] = 0;
-    }
-    if (tid == 0) {
-      *done_counter = 0;
-      if (io.channel_mode) {
-        chan_commit_read(io.ctrl_ch, io.ctrl_ch.rate);
-        chan_commit_read(io.in_ch, io.in_ch.rate);
-        chan_commit_write(io.out_ch, io.out_ch.rate);
-      }
-    }
+    dpd_grid_end<HALO, THREADS>(io, x, period, H1, fast, fs, done_counter, tid);
   }
 }
 
@@ -699,38 +719,7 @@ __global__ void __launch_bounds__(THREADS, DF_DPD_WAVE_MINB)
   float outr[V], outi[V];
 #pragma unroll
   for (int j = 0; j < V; ++j) outr[j] = outi[j] = -0.0f;
-  if (tile == 0 && mask && H1 > 0) {
-    if (tid < 32) {
-      unsigned need = mask;
-      for (long long base = (long long)p; need && base > 0; base -= 32) {
-        const long long idx = base - 1 - tid;
-        const uint32_t m = idx >= 0 ? ctrl[idx] : 0u;
-        for (unsigned bits = need; bits; bits &= bits - 1) {
-          const int b = __ffs(bits);
-          const unsigned bal = __ballot_sync(0xffffffffu, (m >> (b - 1)) & 1u);
-          if (bal) {
-            if (tid == 0) q_s[b - 1] = (int)(base - __ffs(bal));
-            need &= ~(1u << (b - 1));
-          }
-        }
-      }
-      if (tid == 0)
-        for (unsigned bits = need; bits; bits &= bits - 1) q_s[__ffs(bits) - 1] = -1;
-      if (tid < kBranches && ((mask >> tid) & 1u)) atomicMax(&fs.last1[tid], (int)p + 1);
-    }
-    __syncthreads();
-    for (int it = tid; it < kBranches * H1; it += THREADS) {
-      const int bi = it / H1, j = it - bi * H1;
-      if (!((mask >> bi) & 1u)) continue;
-      const int q = q_s[bi];
-      if (q >= 0) {
-        const float2 v = __ldg(&x[(size_t)q * period + (period - 1 - j)]);
-        hist_s[it] = poly_sample(v.x, v.y, bi + 1);
-      } else {
-        hist_s[it] = carried_history<HALO>(fs, bi, j, H1);
-      }
-    }
-  }
+  if (tile == 0 && mask && H1 > 0) dpd_block_history<HALO, THREADS>(ctrl, x, p, mask, period, H1, fs, q_s, hist_s, tid);
   __syncthreads();  // taps_s, hist_s
   const int pt = pad_index(lt);
   const bool has_hist = tile == 0 && tid < H1;
@@ -823,26 +812,7 @@ __global__ void __launch_bounds__(THREADS, DF_DPD_WAVE_MINB)
   __syncthreads();
   if (!last) return;
   __threadfence();
-  for (int it = tid; it < kBranches * H1; it += THREADS) {
-    const int bi = it / H1, j = it - bi * H1;
-    const int q = *(volatile int*)&fs.last1[bi] - 1;
-    if (q >= 0) {
-      const float2 v = x[(size_t)q * period + (period - 1 - j)];
-      fs.state[bi * (kMaxTaps - 1) + j] = poly_sample(v.x, v.y, bi + 1);
-    } else if (HALO && fs.htail[bi]) {
-      fs.state[bi * (kMaxTaps - 1) + j] = carried_history<HALO>(fs, bi, j, H1);
-    }
-  }
-  __syncthreads();
-  if (tid < kBranches) fs.last1[tid] = 0;
-  if (tid == 0) {
-    *done_counter = 0;
-    if (io.channel_mode) {
-      chan_commit_read(io.ctrl_ch, io.ctrl_ch.rate);
-      chan_commit_read(io.in_ch, io.in_ch.rate);
-      chan_commit_write(io.out_ch, io.out_ch.rate);
-    }
-  }
+  dpd_grid_end<HALO, THREADS>(io, x, period, H1, true, fs, done_counter, tid);
 }
 
 // Generic-T fallback (T not 10/32): simple per-output loop, same op order.
