@@ -862,6 +862,9 @@ def main():
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # One line per rank on stderr (the JSON line stays rank 0's only).
+        print(f"bench: rank {rank}/{world} on cuda:{local} ({torch.cuda.get_device_name(local)}), "
+              f"process group {dist.get_backend()}, halo transport {HALO}", file=sys.stderr, flush=True)
     res = (bench_motion_ours if kind == "motion" else bench_dpd_ours)(args, p, rank, world, local)
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
