@@ -877,7 +877,7 @@ def main():
             # (configs[0], [2], [4] per GPU) measured the same way, compactly.
             sec = {}
             sub = argparse.Namespace(**vars(args))
-            sub.steps, sub.warmup = 5, 3
+            sub.steps, sub.warmup = 20, 3  # 20 back-to-back steps (a DPD-1 step is ~10 us)
             for name in ("dpd1", "dpd3", "dpd5"):
                 sub.workload = name
                 r = bench_dpd_ours(sub, WORKLOADS[name][1], rank, world, local)
