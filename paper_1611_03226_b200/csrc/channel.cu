@@ -16,11 +16,22 @@
 #include "channel_host.hpp"
 #include "common.cuh"
 
+#ifndef DF_CHAN_COMMIT_PDL
+#define DF_CHAN_COMMIT_PDL 1
+#endif
+
 namespace df {
 
 namespace {
 
+// Host-endpoint commit: one thread.  Launched with programmatic dependent
+// launch so it becomes resident while the previous kernel (typically the
+// actor firing that produced or consumed the tokens) drains, and lets the
+// next kernel do the same; it touches the control block only after that
+// previous grid has completed (griddepcontrol.wait).
 __global__ void chan_commit_kernel(DevChan c, unsigned n, int is_write) {
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (is_write)
     chan_commit_write(c, n);
   else
@@ -28,6 +39,20 @@ __global__ void chan_commit_kernel(DevChan c, unsigned n, int is_write) {
 }
 
 __global__ void chan_close_kernel(DevChanState* st) { st->closed = 1; }
+
+int launch_commit(const DevChan& c, unsigned n, int is_write, cudaStream_t s) {
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(1);
+  lc.blockDim = dim3(1);
+  lc.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = attr;
+  lc.numAttrs = DF_CHAN_COMMIT_PDL ? 1 : 0;
+  DF_CHECK_CUDA(cudaLaunchKernelEx(&lc, chan_commit_kernel, c, n, is_write));
+  return after_launch("chan_commit_kernel");
+}
 
 __device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
   x += 0x9e3779b97f4a7c15ULL;
@@ -210,8 +235,7 @@ int df_channel_write_end(df_channel* ch, df_region* region, void* stream) {
     DF_CHECK_CUDA(cudaMemcpyAsync(ch->storage, ch->storage + 3ull * ch->rate * ch->token_size,
                                   ch->token_size, cudaMemcpyDeviceToDevice, s));
   }
-  chan_commit_kernel<<<1, 1, 0, s>>>(ch->dev(), (unsigned)region->tokens, 1);
-  DF_TRY(after_launch("chan_commit_kernel"));
+  DF_TRY(launch_commit(ch->dev(), (unsigned)region->tokens, 1, s));
   ch->host_write_phase = (ch->host_write_phase + 1) % chan_phases(ch->has_delay);
   ch->write_serial = 0;
   region->serial = 0;
@@ -253,7 +277,7 @@ int df_channel_read_end(df_channel* ch, df_region* region, void* stream) {
   DF_REQUIRE(region->direction == 0 && region->serial != 0 && region->serial == ch->read_serial,
              DF_ELOGIC, "channel: read_end without matching read_start");
   DF_CHECK_CUDA(cudaSetDevice(ch->device));
-  chan_commit_kernel<<<1, 1, 0, as_stream(stream)>>>(ch->dev(), (unsigned)region->tokens, 0);
+  DF_TRY(launch_commit(ch->dev(), (unsigned)region->tokens, 0, as_stream(stream)));
   DF_TRY(after_launch("chan_commit_kernel"));
   ch->host_read_phase = (ch->host_read_phase + 1) % chan_phases(ch->has_delay);
   ch->read_serial = 0;

@@ -562,13 +562,19 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, DF_MOTION_MINB) motion_fuse
       last = atomicAdd(done_counter, 1u) == gridDim.x * gridDim.y * gridDim.z - 1;
     }
     __syncthreads();
-    if (last && threadIdx.x == 0) {
+    // Three independent commit chains on three threads (the delay channel's
+    // read then write stay on one): each is an atomic round trip.
+    if (last && threadIdx.x < 3) {
       __threadfence();
-      *done_counter = 0;
-      chan_commit_read(io.in_ch, io.in_ch.rate);
-      chan_commit_read(io.delay_ch, 1);
-      chan_commit_write(io.delay_ch, 1);
-      chan_commit_write(io.out_ch, io.out_ch.rate);
+      if (threadIdx.x == 0) {
+        *done_counter = 0;
+        chan_commit_read(io.in_ch, io.in_ch.rate);
+      } else if (threadIdx.x == 1) {
+        chan_commit_read(io.delay_ch, 1);
+        chan_commit_write(io.delay_ch, 1);
+      } else {
+        chan_commit_write(io.out_ch, io.out_ch.rate);
+      }
     }
   }
 }
@@ -618,6 +624,9 @@ constexpr size_t kSmemBytes = sizeof(uint2) * kWarpsPerCta * (kBandRows + 2) * 3
 #endif
 #ifndef DF_M3_ALT
 #define DF_M3_ALT 1  // odd temporal chunks walk backwards (shared boundary frames hit L2)
+#endif
+#ifndef DF_M3_PDL
+#define DF_M3_PDL 1  // programmatic dependent launch (setup overlaps the previous kernel's tail)
 #endif
 constexpr int kM3Warps = DF_M3_WARPS;
 // Band heights R (template parameter): a frame pass fetches rows y0-3 ..
@@ -1014,6 +1023,12 @@ __global__ void __launch_bounds__(32 * kM3Warps, DF_M3_MINB) motion_m3_kernel(co
   // Tasks past the last tile (the grid's last CTA) walk no frames.
   const int f_end = tx0 < g.W ? min(f_begin + g.chunk, g.frames) : f_begin;
 
+#if DF_M3_PDL
+  // Programmatic dependent launch: the next kernel in the stream (e.g. a
+  // sink's commit) may launch now; this grid sets up (TMEM, barriers) and
+  // waits for the previous grid before touching anything it produced.
+  asm volatile("griddepcontrol.launch_dependents;");
+#endif
   unsigned* tmem_slot = reinterpret_cast<unsigned*>(m3_smem + kM3Warps * m3_ring_bytes<FMT>() + kM3Warps * kM3Stages * 8);
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -1037,6 +1052,9 @@ __global__ void __launch_bounds__(32 * kM3Warps, DF_M3_MINB) motion_m3_kernel(co
   st.l2hint = g.l2hint;
   st.H = g.H;
   st.y0 = y0;
+#if DF_M3_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
   // Channel mode: the map covers the input channel's whole storage; the
   // firing's region (resolved from the device phase) starts at frame slot
   // `base` of it.  Raw mode: the map covers exactly the firing's frames.
@@ -1352,12 +1370,24 @@ int launch_m3(df_motion* m, const MotionIO& io, int frames, cudaStream_t s) {
     fprintf(stderr, "motion_m3: R %d, resident %d/SM, grid %ux%ux%u, chunk %d frames, smem %zu\n",
             kM3Heights[best.ri], m->m3_resident[best.ri], grid.x, grid.y, grid.z, g.chunk, m3_smem_bytes<FMT>());
   const size_t smem = m3_smem_bytes<FMT>();
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = grid;
+  lc.blockDim = dim3(32 * kM3Warps);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = attr;
+  lc.numAttrs = DF_M3_PDL ? 1 : 0;
+  cudaError_t le;
   if (best.ri == 0)
-    motion_m3_kernel<FMT, kM3Heights[0]><<<grid, 32 * kM3Warps, smem, s>>>(map, hmap, io, g, m->scratch);
+    le = cudaLaunchKernelEx(&lc, motion_m3_kernel<FMT, kM3Heights[0]>, map, hmap, io, g, m->scratch);
   else if (best.ri == 1)
-    motion_m3_kernel<FMT, kM3Heights[1]><<<grid, 32 * kM3Warps, smem, s>>>(map, hmap, io, g, m->scratch);
+    le = cudaLaunchKernelEx(&lc, motion_m3_kernel<FMT, kM3Heights[1]>, map, hmap, io, g, m->scratch);
   else
-    motion_m3_kernel<FMT, kM3Heights[2]><<<grid, 32 * kM3Warps, smem, s>>>(map, hmap, io, g, m->scratch);
+    le = cudaLaunchKernelEx(&lc, motion_m3_kernel<FMT, kM3Heights[2]>, map, hmap, io, g, m->scratch);
+  DF_CHECK_CUDA(le);
   return after_launch("motion_m3_kernel");
 }
 
