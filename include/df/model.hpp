@@ -103,24 +103,28 @@ class HostFiringContext {
   std::span<std::byte> output(std::size_t i) const { return outputs_.at(i); }
   std::size_t input_tokens(std::size_t i) const { return in_tokens_.at(i); }
   std::size_t output_tokens(std::size_t i) const { return out_tokens_.at(i); }
-  std::size_t input_token_size(std::size_t i) const { return inputs_.at(i).size() / in_tokens_.at(i); }
-  std::size_t output_token_size(std::size_t i) const { return outputs_.at(i).size() / out_tokens_.at(i); }
+  std::size_t input_token_size(std::size_t i) const { return in_token_size_.at(i); }
+  std::size_t output_token_size(std::size_t i) const { return out_token_size_.at(i); }
   std::uint64_t firing_index() const { return firing_index_; }
 
-  // Assembled by the runtime.
+  // Assembled by the runtime.  A dynamic CPU actor's gated port (rate 0
+  // this firing) has 0 tokens and an empty span.
   void bind(std::vector<std::span<const std::byte>> in, std::vector<std::size_t> in_tokens,
-            std::vector<std::span<std::byte>> out, std::vector<std::size_t> out_tokens, std::uint64_t firing) {
+            std::vector<std::size_t> in_token_size, std::vector<std::span<std::byte>> out,
+            std::vector<std::size_t> out_tokens, std::vector<std::size_t> out_token_size, std::uint64_t firing) {
     inputs_ = std::move(in);
     in_tokens_ = std::move(in_tokens);
+    in_token_size_ = std::move(in_token_size);
     outputs_ = std::move(out);
     out_tokens_ = std::move(out_tokens);
+    out_token_size_ = std::move(out_token_size);
     firing_index_ = firing;
   }
 
  private:
   std::vector<std::span<const std::byte>> inputs_;
   std::vector<std::span<std::byte>> outputs_;
-  std::vector<std::size_t> in_tokens_, out_tokens_;
+  std::vector<std::size_t> in_tokens_, out_tokens_, in_token_size_, out_token_size_;
   std::uint64_t firing_index_ = 0;
 };
 
@@ -155,11 +159,14 @@ struct DeviceActor {
 
 // model.hpp:103-108: mandatory fire; optional init / control / finish.
 //   * fire       host-issued GPU actor: enqueues device work per firing;
-//   * host_fire  CPU actor: computes on host spans in stream order (static
-//                rates, host-issued networks);
+//   * host_fire  CPU actor: computes on host spans in stream order
+//                (host-issued networks; a dynamic CPU actor's control token
+//                is read on the host, one stream synchronisation per firing);
 //   * device     device-resident GPU actor (see DeviceActor).
 // control (the reference's signature) is required for a dynamic
-// device-resident actor: it maps one control token to FiringRates and is
+// device-resident actor and a dynamic CPU actor: it maps one control token
+// to FiringRates.  A CPU actor calls it per firing on the host
+// (control_dispatch); a device-resident actor's control is
 // evaluated for every token value v < control_domain (v little-endian in
 // the token's bytes) into the device control table before the run; a
 // result that is not 0-or-r per port (or a throw) makes that token a

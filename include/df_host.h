@@ -85,6 +85,14 @@ int dfh_validate_demo(int which);  /* which: 0..6, see host_abi.cpp */
  * the producer's firing i before the consumer's firing i). */
 int dfh_delay_chain_run(int device, uint32_t token_rate, int sink_first, uint64_t firings, uint64_t* out_host);
 
+/* Dynamic-rate CPU actors (the static-schedule runtime): the reference's
+ * dynamic DPD network shape -- split, two gated branches with frozen state,
+ * adder -- as CPU actors on device channels, int32 tokens, masks cycling
+ * (bit b-1 = branch b active; a mask above 3 is an illegal rate ->
+ * ActorFault).  out_host: firings * rate int32. */
+int dfh_dynamic_cpu_run(int device, const uint32_t* masks, size_t n_masks, uint32_t rate, uint64_t firings,
+                        int32_t* out_host);
+
 /* ---- data formats either side of the path (df/io.hpp, df/dpd.hpp) -------
  * The reference's text and file formats (proj/src/dpd.cpp:393-462
  * parse_schedule / parse_taps; proj/src/bench.cpp:25-97, :173-262 read_file

@@ -330,6 +330,127 @@ int dfh_delay_chain_run(int device, uint32_t rate, int sink_first, uint64_t firi
   });
 }
 
+// The reference's dynamic DPD network shape with CPU actors on device
+// channels (the static-schedule runtime): source -> split (dynamic: its
+// outputs gated by the control token) -> branch1, branch2 (dynamic, gated
+// in and out, each with a running state that stays frozen while gated off)
+// -> adder (dynamic: gated inputs, always one output) -> sink, plus a config
+// actor feeding the four control channels from `masks` (cycling).  Tokens
+// are int32; source firing i emits i*r+1 .. i*r+r; branch b emits
+// x * (b+1) + state_b (state_b += sum of its inputs, wrapping); the adder
+// sums the active inputs.  A mask above 3 makes every control function
+// return an illegal rate (ControlError -> ActorFault).
+int dfh_dynamic_cpu_run(int device, const uint32_t* masks, size_t n_masks, uint32_t rate, uint64_t firings,
+                        int32_t* out_host) {
+  return guarded([&] {
+    using namespace df;
+    if (!masks || !n_masks || !out_host || !rate) throw std::invalid_argument("dfh_dynamic_cpu_run: bad argument");
+    const std::vector<std::uint32_t> sched(masks, masks + n_masks);
+    std::vector<ChannelSpec> chans;
+    for (const char* id : {"src_split", "split_b1", "split_b2", "b1_adder", "b2_adder", "adder_sink"})
+      chans.push_back({id, 4, rate, false, {}});
+    for (const char* id : {"cfg_split", "cfg_b1", "cfg_b2", "cfg_adder"}) chans.push_back({id, 4, 1, false, {}});
+    auto i32 = [](std::span<const std::byte> s) { return reinterpret_cast<const std::int32_t*>(s.data()); };
+    auto o32 = [](std::span<std::byte> s) { return reinterpret_cast<std::int32_t*>(s.data()); };
+    auto mask_of = [](std::span<const std::byte> t) {
+      std::uint32_t m = 0;
+      std::memcpy(&m, t.data(), 4);
+      return m;
+    };
+    const std::uint32_t r = rate;
+    auto gate = [r](std::uint32_t m, unsigned bit) -> std::uint32_t {
+      if (m > 3) return 7;  // not 0 or r: control_dispatch raises ControlError
+      return ((m >> bit) & 1u) ? r : 0u;
+    };
+    std::vector<ActorSpec> actors;
+    ActorBehavior src;
+    src.host_fire = [r](HostFiringContext& ctx) {
+      std::int32_t* o = reinterpret_cast<std::int32_t*>(ctx.output(0).data());
+      for (std::uint32_t t = 0; t < r; ++t) o[t] = static_cast<std::int32_t>(ctx.firing_index() * r + t + 1);
+    };
+    actors.push_back({"source", ActorKind::static_rate, {{PortDirection::output, PortKind::regular, "src_split"}}, src});
+    ActorBehavior cfg;
+    cfg.host_fire = [sched](HostFiringContext& ctx) {
+      const std::uint32_t m = sched[ctx.firing_index() % sched.size()];
+      for (std::size_t o = 0; o < ctx.output_count(); ++o) std::memcpy(ctx.output(o).data(), &m, 4);
+    };
+    actors.push_back({"config", ActorKind::static_rate,
+                      {{PortDirection::output, PortKind::regular, "cfg_split"},
+                       {PortDirection::output, PortKind::regular, "cfg_b1"},
+                       {PortDirection::output, PortKind::regular, "cfg_b2"},
+                       {PortDirection::output, PortKind::regular, "cfg_adder"}},
+                      cfg});
+    ActorBehavior split;
+    split.control = [=](std::span<const std::byte> t) {
+      const std::uint32_t m = mask_of(t);
+      return FiringRates{{m > 3 ? 7u : r, gate(m, 0), gate(m, 1)}};
+    };
+    split.host_fire = [=](HostFiringContext& ctx) {
+      for (std::size_t o = 0; o < ctx.output_count(); ++o)
+        if (ctx.output_tokens(o)) std::memcpy(ctx.output(o).data(), ctx.input(0).data(), ctx.output(o).size());
+    };
+    actors.push_back({"split", ActorKind::dynamic_rate,
+                      {{PortDirection::input, PortKind::control, "cfg_split"},
+                       {PortDirection::input, PortKind::regular, "src_split"},
+                       {PortDirection::output, PortKind::regular, "split_b1"},
+                       {PortDirection::output, PortKind::regular, "split_b2"}},
+                      split});
+    for (unsigned b = 1; b <= 2; ++b) {
+      auto state = std::make_shared<std::int32_t>(0);
+      ActorBehavior br;
+      br.control = [=](std::span<const std::byte> t) {
+        const std::uint32_t g = gate(mask_of(t), b - 1);
+        return FiringRates{{g, g}};
+      };
+      br.host_fire = [=](HostFiringContext& ctx) {
+        if (!ctx.input_tokens(0)) return;  // gated off: no I/O, state frozen
+        const std::int32_t* x = i32(ctx.input(0));
+        std::int32_t* y = o32(ctx.output(0));
+        std::uint32_t s = static_cast<std::uint32_t>(*state);
+        for (std::uint32_t t = 0; t < r; ++t) s += static_cast<std::uint32_t>(x[t]);
+        *state = static_cast<std::int32_t>(s);
+        for (std::uint32_t t = 0; t < r; ++t)
+          y[t] = static_cast<std::int32_t>(static_cast<std::uint32_t>(x[t]) * (b + 1) + s);
+      };
+      const std::string n = std::to_string(b);
+      actors.push_back({"branch" + n, ActorKind::dynamic_rate,
+                        {{PortDirection::input, PortKind::control, "cfg_b" + n},
+                         {PortDirection::input, PortKind::regular, "split_b" + n},
+                         {PortDirection::output, PortKind::regular, "b" + n + "_adder"}},
+                        br});
+    }
+    ActorBehavior adder;
+    adder.control = [=](std::span<const std::byte> t) {
+      const std::uint32_t m = mask_of(t);
+      return FiringRates{{gate(m, 0), gate(m, 1), m > 3 ? 7u : r}};
+    };
+    adder.host_fire = [=](HostFiringContext& ctx) {
+      std::int32_t* y = o32(ctx.output(0));
+      for (std::uint32_t t = 0; t < r; ++t) {
+        std::uint32_t acc = 0;
+        for (std::size_t k = 0; k < ctx.input_count(); ++k)
+          if (ctx.input_tokens(k)) acc += static_cast<std::uint32_t>(i32(ctx.input(k))[t]);
+        y[t] = static_cast<std::int32_t>(acc);
+      }
+    };
+    actors.push_back({"adder", ActorKind::dynamic_rate,
+                      {{PortDirection::input, PortKind::control, "cfg_adder"},
+                       {PortDirection::input, PortKind::regular, "b1_adder"},
+                       {PortDirection::input, PortKind::regular, "b2_adder"},
+                       {PortDirection::output, PortKind::regular, "adder_sink"}},
+                      adder});
+    ActorBehavior sink;
+    sink.host_fire = [=](HostFiringContext& ctx) {
+      std::memcpy(out_host + ctx.firing_index() * r, ctx.input(0).data(), 4ull * r);
+    };
+    actors.push_back({"sink", ActorKind::static_rate, {{PortDirection::input, PortKind::regular, "adder_sink"}}, sink});
+    ExecutionConfig ec;
+    ec.device = device;
+    ec.source_firing_limit = firings;
+    run(build_network(actors, chans), ec);
+  });
+}
+
 int dfh_validate_demo(int which) {
   int n = -1;
   int rc = guarded([&] {

@@ -66,7 +66,13 @@ struct ActorRun {
   // regular port (token_size * rate bytes).  Firings of one actor are
   // serialised on its stream, so one copy per port suffices.
   std::vector<std::byte*> stage_in, stage_out;
-  std::vector<std::size_t> bytes_in, bytes_out, tokens_in, tokens_out;
+  std::vector<std::size_t> bytes_in, bytes_out, tokens_in, tokens_out, tsize_in, tsize_out;
+  // Dynamic CPU actors: the actor's index, its control token's host copy,
+  // and regular port k (declaration order) -> (is input, index).
+  std::size_t index = 0;
+  std::byte* stage_ctrl = nullptr;
+  std::size_t ctrl_bytes = 0;
+  std::vector<std::pair<bool, std::size_t>> regular_ports;
 };
 
 // Fault raised inside a CPU actor's host_fire (which runs on a CUDA
@@ -83,6 +89,8 @@ struct HostJob {
   HostFaults* faults;
   const ActorRun* run;
   std::uint64_t firing;
+  // This firing's tokens per port (0 on a dynamic actor's gated ports).
+  std::vector<std::size_t> tokens_in, tokens_out;
 };
 
 void host_job_entry(void* p) {
@@ -92,10 +100,11 @@ void host_job_entry(void* p) {
   try {
     std::vector<std::span<const std::byte>> in;
     std::vector<std::span<std::byte>> out;
-    for (std::size_t k = 0; k < r.stage_in.size(); ++k) in.emplace_back(r.stage_in[k], r.bytes_in[k]);
-    for (std::size_t k = 0; k < r.stage_out.size(); ++k) out.emplace_back(r.stage_out[k], r.bytes_out[k]);
+    for (std::size_t k = 0; k < r.stage_in.size(); ++k) in.emplace_back(r.stage_in[k], job.tokens_in[k] * r.tsize_in[k]);
+    for (std::size_t k = 0; k < r.stage_out.size(); ++k)
+      out.emplace_back(r.stage_out[k], job.tokens_out[k] * r.tsize_out[k]);
     HostFiringContext ctx;
-    ctx.bind(std::move(in), r.tokens_in, std::move(out), r.tokens_out, job.firing);
+    ctx.bind(std::move(in), job.tokens_in, r.tsize_in, std::move(out), job.tokens_out, r.tsize_out, job.firing);
     r.spec->behavior.host_fire(ctx);
   } catch (const std::exception& e) {
     std::lock_guard<std::mutex> lock(job.faults->mu);
@@ -113,22 +122,48 @@ void host_job_entry(void* p) {
 }
 
 // One firing of a CPU actor, all in its stream: inputs' regions D2H, the
-// host function, outputs' regions H2D, then the channel commits.
-void fire_host_actor(ActorRun& r, std::uint64_t firing, HostFaults& faults, std::deque<HostJob>& jobs) {
+// host function, outputs' regions H2D, then the channel commits.  A dynamic
+// CPU actor first reads its control token: the token's D2H copy is waited
+// for on the host (one stream synchronisation per firing -- the reference's
+// actor thread blocks on its control channel the same way,
+// runtime.cpp:139-145), control_dispatch turns it into 0-or-r rates
+// (ControlError -> ActorFault), and only the active ports' regions move and
+// commit.  The host mirror of each endpoint's phase advances with its own
+// commits only, so it stays exact.
+void fire_host_actor(const NetworkGraph& net, ActorRun& r, std::uint64_t firing, HostFaults& faults,
+                     std::deque<HostJob>& jobs) {
   const std::size_t nin = r.ctx.input_count(), nout = r.ctx.output_count();
+  std::vector<std::size_t> tin = r.tokens_in, tout = r.tokens_out;
+  df_region rc{};
+  if (r.ctx.control()) {
+    check(df_channel_read_start(r.ctx.control(), 1, &rc));
+    check(df_memcpy_d2h(r.stage_ctrl, rc.dptr, r.ctrl_bytes, r.stream));
+    check(df_stream_synchronize(r.stream));
+    const FiringRates rates =
+        control_dispatch(net, r.index, std::span<const std::byte>(r.stage_ctrl, r.ctrl_bytes));
+    for (std::size_t k = 0; k < r.regular_ports.size(); ++k) {
+      const auto [is_in, idx] = r.regular_ports[k];
+      (is_in ? tin : tout)[idx] = rates.by_regular_port[k];
+    }
+  }
   std::vector<df_region> rin(nin), rout(nout);
   for (std::size_t k = 0; k < nin; ++k) {
-    check(df_channel_read_start(r.ctx.input(k), r.tokens_in[k], &rin[k]));
+    if (!tin[k]) continue;
+    check(df_channel_read_start(r.ctx.input(k), tin[k], &rin[k]));
     check(df_memcpy_d2h(r.stage_in[k], rin[k].dptr, r.bytes_in[k], r.stream));
   }
-  for (std::size_t k = 0; k < nout; ++k) check(df_channel_write_start(r.ctx.output(k), r.tokens_out[k], &rout[k]));
-  jobs.push_back({&faults, &r, firing});
+  for (std::size_t k = 0; k < nout; ++k)
+    if (tout[k]) check(df_channel_write_start(r.ctx.output(k), tout[k], &rout[k]));
+  jobs.push_back({&faults, &r, firing, tin, tout});
   check(df_launch_host_func(r.stream, host_job_entry, &jobs.back()));
   for (std::size_t k = 0; k < nout; ++k) {
+    if (!tout[k]) continue;
     check(df_memcpy_h2d(rout[k].dptr, r.stage_out[k], r.bytes_out[k], r.stream));
     check(df_channel_write_end(r.ctx.output(k), &rout[k], r.stream));
   }
-  for (std::size_t k = 0; k < nin; ++k) check(df_channel_read_end(r.ctx.input(k), &rin[k], r.stream));
+  for (std::size_t k = 0; k < nin; ++k)
+    if (tin[k]) check(df_channel_read_end(r.ctx.input(k), &rin[k], r.stream));
+  if (r.ctx.control()) check(df_channel_read_end(r.ctx.control(), &rc, r.stream));
 }
 
 // Device-resident run: every actor fires inside one persistent kernel
@@ -293,6 +328,7 @@ RunStats run(const NetworkGraph& net, const ExecutionConfig& cfg) {
       if (r.stream) df_stream_synchronize(r.stream);  // host callbacks may still reference the stages
       for (std::byte* b : r.stage_in) df_host_free(b);
       for (std::byte* b : r.stage_out) df_host_free(b);
+      if (r.stage_ctrl) df_host_free(r.stage_ctrl);
       for (void*& e : r.done)
         if (e) df_event_destroy(e);
       if (r.t_first) df_event_destroy(r.t_first);
@@ -330,16 +366,29 @@ RunStats run(const NetworkGraph& net, const ExecutionConfig& cfg) {
       }
       if (r.spec->behavior.is_host()) {
         auto stage = [&](df_channel* ch, std::vector<std::byte*>& bufs, std::vector<std::size_t>& bytes,
-                         std::vector<std::size_t>& tokens) {
+                         std::vector<std::size_t>& tokens, std::vector<std::size_t>& tsize) {
           const std::size_t n = df_channel_token_rate(ch), b = n * df_channel_token_size(ch);
           void* h = nullptr;
           check(df_host_alloc(b, &h));
           bufs.push_back(static_cast<std::byte*>(h));
           bytes.push_back(b);
           tokens.push_back(n);
+          tsize.push_back(df_channel_token_size(ch));
         };
-        for (df_channel* ch : in) stage(ch, r.stage_in, r.bytes_in, r.tokens_in);
-        for (df_channel* ch : out) stage(ch, r.stage_out, r.bytes_out, r.tokens_out);
+        for (df_channel* ch : in) stage(ch, r.stage_in, r.bytes_in, r.tokens_in, r.tsize_in);
+        for (df_channel* ch : out) stage(ch, r.stage_out, r.bytes_out, r.tokens_out, r.tsize_out);
+        r.index = a;
+        if (ctrl) {  // dynamic CPU actor: its control token's host copy
+          r.ctrl_bytes = df_channel_token_size(ctrl);
+          void* h = nullptr;
+          check(df_host_alloc(r.ctrl_bytes, &h));
+          r.stage_ctrl = static_cast<std::byte*>(h);
+          std::size_t ni = 0, no = 0;
+          for (const PortSpec& port : r.spec->ports)
+            if (port.kind == PortKind::regular)
+              r.regular_ports.push_back(port.direction == PortDirection::input ? std::make_pair(true, ni++)
+                                                                               : std::make_pair(false, no++));
+        }
       }
       r.ctx.bind(std::move(in), std::move(out), ctrl);
     }
@@ -383,7 +432,7 @@ RunStats run(const NetworkGraph& net, const ExecutionConfig& cfg) {
         fault_actor = r.spec->id;
         nvtxRangePushA(r.spec->id.c_str());  // the enqueue of firing i (host timeline)
         if (r.spec->behavior.is_host())
-          fire_host_actor(r, i, host_faults, host_jobs);
+          fire_host_actor(net, r, i, host_faults, host_jobs);
         else
           r.spec->behavior.fire(r.ctx);
         nvtxRangePop();

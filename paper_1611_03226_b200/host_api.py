@@ -51,6 +51,7 @@ def lib():
                                           C.POINTER(C.c_uint64)]
         L.dfh_read_cf32.argtypes = [C.c_char_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_uint64)]
         L.dfh_write_file.argtypes = [C.c_char_p, C.c_void_p, C.c_size_t]
+        L.dfh_dynamic_cpu_run.argtypes = [C.c_int, C.c_void_p, C.c_size_t, C.c_uint32, C.c_uint64, C.c_void_p]
         _h = L
     return _h
 
@@ -223,3 +224,12 @@ def read_cf32(path: str) -> np.ndarray:
 def write_file(path: str, data: np.ndarray):
     data = np.ascontiguousarray(data)
     _check(lib().dfh_write_file(os.fsencode(path), data.ctypes.data_as(C.c_void_p), data.nbytes))
+
+
+def dynamic_cpu_run(masks, rate: int, firings: int, device: int = 0) -> np.ndarray:
+    """The dynamic DPD network shape as CPU actors (dfh_dynamic_cpu_run): int32 [firings * rate]."""
+    m = np.ascontiguousarray(masks, np.uint32)
+    out = np.empty(firings * rate, np.int32)
+    _check(lib().dfh_dynamic_cpu_run(device, m.ctypes.data_as(C.c_void_p), m.size, rate, firings,
+                                     out.ctypes.data_as(C.c_void_p)))
+    return out

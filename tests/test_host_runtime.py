@@ -30,8 +30,8 @@ def test_unknown_channel_is_build_error():
 
 
 def test_validate_cpu_actor_rules():
-    # A dynamic CPU actor (control tokens are consumed on the device, GPU
-    # actors only) and an actor with both a host and a device fire function.
+    # A CPU actor marked device_control (a CPU actor reads its control token
+    # on the host) and an actor with both a host and a device fire function.
     assert H.validate_demo(4) == 2
 
 

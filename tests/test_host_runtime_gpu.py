@@ -108,3 +108,39 @@ def test_delay_channel_orders_firings(gpu, rate, sink_first):
     got = H.delay_chain_run(rate, sink_first, firings)
     want = np.concatenate([[np.uint64(2**64 - 1)], np.arange(1, firings * rate, dtype=np.uint64)])
     np.testing.assert_array_equal(got, want)
+
+
+def _dynamic_cpu_expected(masks, rate, firings):
+    # split -> branch b (x*(b+1) + running state, frozen while gated off) -> adder, int32 wrapping
+    state = [0, 0]
+    out = np.zeros(firings * rate, np.uint32)
+    for i in range(firings):
+        m = masks[i % len(masks)]
+        x = (np.arange(rate, dtype=np.uint64) + i * rate + 1).astype(np.uint32)
+        acc = np.zeros(rate, np.uint32)
+        for b in (1, 2):
+            if (m >> (b - 1)) & 1:
+                state[b - 1] = (state[b - 1] + int(x.astype(np.uint64).sum())) & 0xFFFFFFFF
+                acc += x * np.uint32(b + 1) + np.uint32(state[b - 1])
+        out[i * rate:(i + 1) * rate] = acc
+    return out.view(np.int32)
+
+
+@pytest.mark.parametrize("rate", [1, 3])
+def test_dynamic_cpu_actors_gated_ports_and_frozen_state(gpu, rate):
+    # Dynamic-rate CPU actors (control read on the host, 0-or-r per port): the
+    # reference's dynamic split / branch / adder shape with matched gating,
+    # branches gated off for stretches (their state must stay frozen), and a
+    # mask with no branch active (the adder still produces).
+    from paper_1611_03226_b200 import host_api as H
+    masks = [3, 1, 1, 0, 2, 3, 2, 2, 1]
+    firings = 23
+    got = H.dynamic_cpu_run(masks, rate, firings)
+    np.testing.assert_array_equal(got, _dynamic_cpu_expected(masks, rate, firings))
+
+
+def test_dynamic_cpu_actor_illegal_rate_is_actor_fault(gpu):
+    from paper_1611_03226_b200 import host_api as H
+    with pytest.raises(H.HostRunError) as e:
+        H.dynamic_cpu_run([3, 1, 9], 2, 6)
+    assert "ActorFault" in str(e.value) and "control" in str(e.value)
