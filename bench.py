@@ -813,7 +813,7 @@ def resident_networks():
                              "32 CTAs per branch"},
             "motion720gray": {"value": round(300 / (statistics.median(mm) / 1e3), 1), "unit": "frames/s",
                               "path": "dfh_motion_run_resident: source, gauss, thres, med, sink with the "
-                                      "gauss_thres_prev delay channel, 96 CTAs per actor"},
+                                      "gauss_thres_prev delay channel, 480 CTAs shared by work (gauss 160, med 120, thres 80, source / sink 60)"},
             "metric": "units / sink-active seconds (bench.cpp:341-347, :391-397), device timestamps"}
 
 

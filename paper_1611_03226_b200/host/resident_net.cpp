@@ -10,6 +10,7 @@
 // token on the device.
 // Motion: /root/reference/proj/src/motion.cpp:107-218 -- source, gauss,
 // thres, med, sink with the one-frame delay channel gauss_thres_prev.
+#include <algorithm>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -220,16 +221,21 @@ NetworkGraph build_reference_network(const Params& p, int device, std::uint32_t 
   df_act_frames sp = fp, kp = fp;
   sp.frames = d_in;
   kp.frames = d_out;
-  source.device = DeviceActor::of(DF_ACT_FRAME_SOURCE, sp, ctas);
+  // `ctas` is the mean per actor: the group sizes follow each actor's work
+  // per frame (gauss 15 loads per 4 px, median 5 + a sorting network, thres
+  // 2, source / sink a copy), so the 5 * ctas CTAs of one wave are spent where
+  // the firing time is (DF_NET_PROFILE: fire times 1 : 0.77 : 0.52 : 0.3).
+  auto share = [ctas](std::uint32_t num, std::uint32_t den) { return std::max<std::uint32_t>(1, ctas * num / den); };
+  source.device = DeviceActor::of(DF_ACT_FRAME_SOURCE, sp, share(5, 8));
   const auto input = p.input;
   source.init = [buf, d_in, input, bytes] {
     check(df_memcpy_h2d(d_in, input.data(), bytes, nullptr));
     check(df_stream_synchronize(nullptr));
   };
-  gauss.device = DeviceActor::of(DF_ACT_GAUSS, fp, ctas);
-  thres.device = DeviceActor::of(DF_ACT_THRES, fp, ctas);
-  med.device = DeviceActor::of(DF_ACT_MEDIAN, fp, ctas);
-  sink.device = DeviceActor::of(DF_ACT_FRAME_SINK, kp, ctas);
+  gauss.device = DeviceActor::of(DF_ACT_GAUSS, fp, share(5, 3));
+  thres.device = DeviceActor::of(DF_ACT_THRES, fp, share(5, 6));
+  med.device = DeviceActor::of(DF_ACT_MEDIAN, fp, share(5, 4));
+  sink.device = DeviceActor::of(DF_ACT_FRAME_SINK, kp, share(5, 8));
   const auto output = p.output;
   sink.finish = [buf, d_out, output, bytes] {
     check(df_memcpy_d2h(output.data(), d_out, bytes, nullptr));
