@@ -93,7 +93,7 @@ NetworkGraph build_reference_network(const Params& p, int device, std::uint32_t 
   auto ctl = [](const std::string& c) { return PortSpec{PortDirection::input, PortKind::control, c}; };
   std::vector<ActorSpec> actors;
 
-  const std::uint32_t io_ctas = std::max<std::uint32_t>(1, branch_ctas / 2);
+  const std::uint32_t io_ctas = std::max<std::uint32_t>(1, branch_ctas);
   ActorBehavior source;  // dpd.cpp:189-204 (input staged to HBM before the run)
   source.device = DeviceActor::of(DF_ACT_DPD_SOURCE, df_act_samples{d_in, period}, io_ctas);
   const auto input = p.input;
