@@ -30,7 +30,14 @@ struct ConfigToken {
   unsigned active_count() const { return __builtin_popcount(active_mask); }
   bool active(unsigned branch) const { return (active_mask >> (branch - 1)) & 1u; }
   static ConfigToken first_n(unsigned k) { return {static_cast<std::uint16_t>((1u << k) - 1)}; }
+  bool operator==(const ConfigToken&) const = default;
 };
+
+// dpd.hpp:37-41: the wire form of a config token, 4 bytes little endian --
+// what the config actor writes and the GPU actor reads on the device.
+inline constexpr std::size_t kConfigTokenBytes = 4;
+void encode_config(ConfigToken token, std::span<std::byte> out);
+ConfigToken decode_config(std::span<const std::byte> in);
 
 // check_config (dpd.cpp:49-58): k in [min_active, 10], no branch beyond
 // 10.  The reference's bound is k >= 2 (the default); min_active = 1 is the

@@ -100,6 +100,9 @@ int dfh_dynamic_cpu_run(int device, const uint32_t* masks, size_t n_masks, uint3
  * FormatError (the reference's ConfigError: unreadable, truncated or
  * malformed file); parse errors are status 6 with the reference's message.
  * Size queries: pass a NULL buffer to get the sizes, then call again. */
+/* The config token's wire form (dpd.cpp:38-47): 4 bytes little endian. */
+int dfh_encode_config(uint16_t mask, uint8_t* out4);
+int dfh_decode_config(const uint8_t* in4, uint16_t* mask);
 int dfh_parse_schedule(const char* text, uint16_t* masks, size_t cap, size_t* count);
 int dfh_parse_taps(const char* text, uint32_t taps_per_branch, float* taps_out /* 10*T*2 floats */);
 int dfh_read_pgm(const char* path, uint8_t* pixels, size_t cap_bytes, unsigned* width, unsigned* height,

@@ -10,6 +10,19 @@
 
 namespace df::dpd {
 
+void encode_config(ConfigToken token, std::span<std::byte> out) {  // dpd.cpp:38-41
+  if (out.size() < kConfigTokenBytes) throw std::invalid_argument("config token needs 4 bytes");
+  const std::uint32_t v = token.active_mask;
+  for (std::size_t i = 0; i < kConfigTokenBytes; ++i) out[i] = static_cast<std::byte>((v >> (8 * i)) & 0xFF);
+}
+
+ConfigToken decode_config(std::span<const std::byte> in) {  // dpd.cpp:43-47 (bits above 15 are dropped)
+  if (in.size() < kConfigTokenBytes) throw std::invalid_argument("config token needs 4 bytes");
+  std::uint32_t v = 0;
+  for (std::size_t i = 0; i < kConfigTokenBytes; ++i) v |= static_cast<std::uint32_t>(in[i]) << (8 * i);
+  return {static_cast<std::uint16_t>(v)};
+}
+
 void check_config(ConfigToken token, unsigned min_active) {
   // dpd.cpp:49-58 (the reference network requires k >= 2; k = 1 is the
   // north-star extension, its oracle accepts any mask; see dpd.hpp)

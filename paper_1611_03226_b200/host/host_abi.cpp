@@ -556,6 +556,20 @@ int dfh_validate_demo(int which) {
 }
 
 
+int dfh_encode_config(uint16_t mask, uint8_t* out4) {
+  return guarded([&] {
+    if (!out4) throw std::invalid_argument("dfh_encode_config: null argument");
+    df::dpd::encode_config({mask}, std::span<std::byte>(reinterpret_cast<std::byte*>(out4), 4));
+  });
+}
+
+int dfh_decode_config(const uint8_t* in4, uint16_t* mask) {
+  return guarded([&] {
+    if (!in4 || !mask) throw std::invalid_argument("dfh_decode_config: null argument");
+    *mask = df::dpd::decode_config(std::span<const std::byte>(reinterpret_cast<const std::byte*>(in4), 4)).active_mask;
+  });
+}
+
 int dfh_parse_schedule(const char* text, uint16_t* masks, size_t cap, size_t* count) {
   return guarded([&] {
     if (!text || !count) throw std::invalid_argument("dfh_parse_schedule: null argument");

@@ -51,6 +51,8 @@ def lib():
                                           C.POINTER(C.c_uint64)]
         L.dfh_read_cf32.argtypes = [C.c_char_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_uint64)]
         L.dfh_write_file.argtypes = [C.c_char_p, C.c_void_p, C.c_size_t]
+        L.dfh_encode_config.argtypes = [C.c_uint16, C.c_void_p]
+        L.dfh_decode_config.argtypes = [C.c_void_p, C.POINTER(C.c_uint16)]
         L.dfh_dynamic_cpu_run.argtypes = [C.c_int, C.c_void_p, C.c_size_t, C.c_uint32, C.c_uint64, C.c_void_p]
         _h = L
     return _h
@@ -233,3 +235,16 @@ def dynamic_cpu_run(masks, rate: int, firings: int, device: int = 0) -> np.ndarr
     _check(lib().dfh_dynamic_cpu_run(device, m.ctypes.data_as(C.c_void_p), m.size, rate, firings,
                                      out.ctypes.data_as(C.c_void_p)))
     return out
+
+
+def encode_config(mask: int) -> bytes:
+    out = (C.c_uint8 * 4)()
+    _check(lib().dfh_encode_config(mask, out))
+    return bytes(out)
+
+
+def decode_config(b: bytes) -> int:
+    buf = (C.c_uint8 * 4).from_buffer_copy(b[:4])
+    m = C.c_uint16()
+    _check(lib().dfh_decode_config(buf, C.byref(m)))
+    return m.value

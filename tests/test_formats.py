@@ -154,3 +154,11 @@ def test_raw_frames_and_cf32(tmp_path):
     with pytest.raises(H.HostRunError) as e:
         H.read_cf32(str(tmp_path / "odd.cf32"))
     assert "interleaved float re,im pairs" in str(e.value)
+
+
+def test_config_token_wire_form():
+    # dpd.cpp:38-47: 4 bytes little endian; decode keeps the low 16 bits
+    for m in (0x3, 0x3FF, 0x155, 0x8001):
+        assert H.encode_config(m) == m.to_bytes(4, "little")
+        assert H.decode_config(m.to_bytes(4, "little")) == m
+    assert H.decode_config((0x12345).to_bytes(4, "little")) == 0x2345
