@@ -66,6 +66,13 @@ struct Params {
 std::vector<ConfigToken> parse_schedule(std::istream& in);
 std::vector<std::complex<float>> parse_taps(std::istream& in, unsigned taps_per_branch = 10);
 
+// The reference's generators (dpd.hpp:122-124; host/generators.cpp):
+// schedules of 2..10 branches, taps in [-0.5, 0.5) (10 x T, branch-major),
+// samples in [-1, 1), all from std::mt19937_64(seed) as the reference draws.
+std::vector<ConfigToken> random_schedule(std::size_t entries, std::uint64_t seed);
+std::vector<std::complex<float>> random_taps(std::uint64_t seed, unsigned taps_per_branch = 10);
+std::vector<std::complex<float>> synth_samples(std::uint64_t samples, std::uint64_t seed);
+
 NetworkGraph build_network(const Params& params);
 std::uint64_t source_firings(const Params& params);  // launches
 

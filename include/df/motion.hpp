@@ -50,4 +50,8 @@ struct MixedParams {
 };
 NetworkGraph build_mixed_network(const MixedParams& params);
 
+// The reference's frame generator (motion.hpp:77, motion.cpp:254-260):
+// one byte per draw of std::mt19937_64(seed).
+std::vector<std::uint8_t> synth_frames(std::uint64_t frames, unsigned width, unsigned height, std::uint64_t seed);
+
 }  // namespace df::motion

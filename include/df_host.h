@@ -100,6 +100,11 @@ int dfh_dynamic_cpu_run(int device, const uint32_t* masks, size_t n_masks, uint3
  * FormatError (the reference's ConfigError: unreadable, truncated or
  * malformed file); parse errors are status 6 with the reference's message.
  * Size queries: pass a NULL buffer to get the sizes, then call again. */
+/* The reference's generators (df::dpd::random_schedule / random_taps /
+ * synth_samples, df::motion::synth_frames): what 0 = n uint16 schedule
+ * masks, 1 = 10 x n complex taps, 2 = n complex samples, 3 = n frame bytes. */
+int dfh_synth(int what, uint64_t n, uint64_t seed, void* out);
+
 /* The config token's wire form (dpd.cpp:38-47): 4 bytes little endian. */
 int dfh_encode_config(uint16_t mask, uint8_t* out4);
 int dfh_decode_config(const uint8_t* in4, uint16_t* mask);

@@ -556,6 +556,27 @@ int dfh_validate_demo(int which) {
 }
 
 
+int dfh_synth(int what, uint64_t n, uint64_t seed, void* out) {
+  return guarded([&] {
+    if (!out) throw std::invalid_argument("dfh_synth: null output");
+    if (what == 0) {  // schedule: n uint16 masks
+      const auto v = df::dpd::random_schedule(n, seed);
+      for (std::size_t i = 0; i < v.size(); ++i) static_cast<uint16_t*>(out)[i] = v[i].active_mask;
+    } else if (what == 1) {  // taps: 10 x n complex
+      const auto v = df::dpd::random_taps(seed, static_cast<unsigned>(n));
+      std::memcpy(out, v.data(), v.size() * sizeof(v[0]));
+    } else if (what == 2) {  // n complex samples
+      const auto v = df::dpd::synth_samples(n, seed);
+      std::memcpy(out, v.data(), v.size() * sizeof(v[0]));
+    } else if (what == 3) {  // n frame bytes (frames * W * H)
+      const auto v = df::motion::synth_frames(n, 1, 1, seed);
+      std::memcpy(out, v.data(), v.size());
+    } else {
+      throw std::invalid_argument("dfh_synth: unknown generator");
+    }
+  });
+}
+
 int dfh_encode_config(uint16_t mask, uint8_t* out4) {
   return guarded([&] {
     if (!out4) throw std::invalid_argument("dfh_encode_config: null argument");

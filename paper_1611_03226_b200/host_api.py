@@ -51,6 +51,7 @@ def lib():
                                           C.POINTER(C.c_uint64)]
         L.dfh_read_cf32.argtypes = [C.c_char_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_uint64)]
         L.dfh_write_file.argtypes = [C.c_char_p, C.c_void_p, C.c_size_t]
+        L.dfh_synth.argtypes = [C.c_int, C.c_uint64, C.c_uint64, C.c_void_p]
         L.dfh_encode_config.argtypes = [C.c_uint16, C.c_void_p]
         L.dfh_decode_config.argtypes = [C.c_void_p, C.POINTER(C.c_uint16)]
         L.dfh_dynamic_cpu_run.argtypes = [C.c_int, C.c_void_p, C.c_size_t, C.c_uint32, C.c_uint64, C.c_void_p]
@@ -248,3 +249,12 @@ def decode_config(b: bytes) -> int:
     m = C.c_uint16()
     _check(lib().dfh_decode_config(buf, C.byref(m)))
     return m.value
+
+
+def synth(what: str, n: int, seed: int) -> np.ndarray:
+    """The library's copies of the reference's generators (dfh_synth)."""
+    kind, dtype, count = {"schedule": (0, np.uint16, n), "taps": (1, np.float32, 20 * n),
+                          "samples": (2, np.float32, 2 * n), "frames": (3, np.uint8, n)}[what]
+    out = np.empty(count, dtype)
+    _check(lib().dfh_synth(kind, n, seed, out.ctypes.data_as(C.c_void_p)))
+    return out

@@ -162,3 +162,16 @@ def test_config_token_wire_form():
         assert H.encode_config(m) == m.to_bytes(4, "little")
         assert H.decode_config(m.to_bytes(4, "little")) == m
     assert H.decode_config((0x12345).to_bytes(4, "little")) == 0x2345
+
+
+def test_library_generators_match_the_reference_streams(hashes):
+    # df::dpd::random_schedule / random_taps / synth_samples and
+    # df::motion::synth_frames against the reference's own streams (golden
+    # values recorded from the compiled reference, tests/golden).
+    import hashlib
+    g = hashes["generators"]
+    assert H.synth("taps", 10, 808).tolist() == g["taps808"]
+    assert H.synth("schedule", 16, 809).tolist() == g["sched16_809"]
+    assert H.synth("frames", 320 * 240, 606)[:64].tolist() == g["frames_606_first64"]
+    x = H.synth("samples", 1 << 20, 810)
+    assert hashlib.sha256(x.tobytes()).hexdigest() == hashes["dpd_acceptance8"]["input_sha256"]
