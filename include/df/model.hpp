@@ -220,6 +220,7 @@ class NetworkGraph {
   const std::vector<ChannelEndpoints>& endpoints() const { return endpoints_; }
   std::size_t actor_index(const std::string& id) const;
   std::size_t channel_index(const std::string& id) const;
+  const ChannelSpec& channel(const std::string& id) const { return channels().at(channel_index(id)); }  // model.hpp:158
   std::vector<std::size_t> regular_ports(std::size_t actor) const;
   std::optional<std::size_t> control_port(std::size_t actor) const;
 

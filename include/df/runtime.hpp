@@ -22,6 +22,7 @@
 // control tokens naming a branch beyond 10) surface as ActorFault.
 #pragma once
 
+#include <functional>
 #include <chrono>
 #include <cstdint>
 #include <optional>
@@ -98,6 +99,14 @@ class RunAborted : public std::runtime_error {
 //     as a static schedule (the actors fire in lock step), synchronizes;
 // then runs finish, checks device-side errors and returns the stats.
 RunStats run(const NetworkGraph& net, const ExecutionConfig& cfg);
+
+// runtime.hpp:97-108: a batch function mirroring a kernel invocation -- one
+// contiguous input array per regular input port, one produced array per
+// regular output port -- wrapped as a CPU actor (host_fire) that hands it
+// whole r-token regions.  Wrong output count or size faults the actor.
+using BatchKernel =
+    std::function<std::vector<std::vector<std::byte>>(const std::vector<std::span<const std::byte>>&)>;
+ActorBehavior bulk_kernel_adapter(BatchKernel kernel);
 
 // Throws the C++ exception matching a df_* status (DF_EINVAL ->
 // std::invalid_argument, DF_ELOGIC -> std::logic_error, DF_EABORTED ->

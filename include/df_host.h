@@ -93,6 +93,11 @@ int dfh_delay_chain_run(int device, uint32_t token_rate, int sink_first, uint64_
 int dfh_dynamic_cpu_run(int device, const uint32_t* masks, size_t n_masks, uint32_t rate, uint64_t firings,
                         int32_t* out_host);
 
+/* df::bulk_kernel_adapter (runtime.hpp:97-108): source -> a CPU actor made
+ * from a batch kernel (int32 x -> 2x; bad != 0: a wrong output size, which
+ * faults the actor) -> sink.  out_host: firings * rate int32. */
+int dfh_bulk_kernel_run(int device, uint32_t rate, uint64_t firings, int bad, int32_t* out_host);
+
 /* ---- data formats either side of the path (df/io.hpp, df/dpd.hpp) -------
  * The reference's text and file formats (proj/src/dpd.cpp:393-462
  * parse_schedule / parse_taps; proj/src/bench.cpp:25-97, :173-262 read_file

@@ -451,6 +451,42 @@ int dfh_dynamic_cpu_run(int device, const uint32_t* masks, size_t n_masks, uint3
   });
 }
 
+// source (CPU) -> doubler (bulk_kernel_adapter: int32 x -> 2x, or a wrong
+// output size when bad) -> sink (CPU); out_host: firings * rate int32.
+int dfh_bulk_kernel_run(int device, uint32_t rate, uint64_t firings, int bad, int32_t* out_host) {
+  return guarded([&] {
+    using namespace df;
+    if (!out_host || !rate) throw std::invalid_argument("dfh_bulk_kernel_run: bad argument");
+    std::vector<ChannelSpec> chans = {{"a", 4, rate, false, {}}, {"b", 4, rate, false, {}}};
+    ActorBehavior src, snk;
+    src.host_fire = [rate](HostFiringContext& ctx) {
+      auto* o = reinterpret_cast<std::int32_t*>(ctx.output(0).data());
+      for (std::uint32_t t = 0; t < rate; ++t) o[t] = static_cast<std::int32_t>(ctx.firing_index() * rate + t);
+    };
+    snk.host_fire = [out_host, rate](HostFiringContext& ctx) {
+      std::memcpy(out_host + ctx.firing_index() * rate, ctx.input(0).data(), 4ull * rate);
+    };
+    ActorBehavior dbl = bulk_kernel_adapter([bad](const std::vector<std::span<const std::byte>>& in) {
+      const auto* x = reinterpret_cast<const std::int32_t*>(in[0].data());
+      std::vector<std::byte> y(in[0].size() + (bad ? 4 : 0));
+      for (std::size_t t = 0; t < in[0].size() / 4; ++t) {
+        const std::int32_t v = 2 * x[t];
+        std::memcpy(y.data() + 4 * t, &v, 4);
+      }
+      return std::vector<std::vector<std::byte>>{std::move(y)};
+    });
+    std::vector<ActorSpec> actors = {
+        {"source", ActorKind::static_rate, {{PortDirection::output, PortKind::regular, "a"}}, src},
+        {"doubler", ActorKind::static_rate,
+         {{PortDirection::input, PortKind::regular, "a"}, {PortDirection::output, PortKind::regular, "b"}}, dbl},
+        {"sink", ActorKind::static_rate, {{PortDirection::input, PortKind::regular, "b"}}, snk}};
+    ExecutionConfig ec;
+    ec.device = device;
+    ec.source_firing_limit = firings;
+    run(build_network(actors, chans), ec);
+  });
+}
+
 int dfh_validate_demo(int which) {
   int n = -1;
   int rc = guarded([&] {

@@ -308,6 +308,27 @@ RunStats run_device(const NetworkGraph& net, const ExecutionConfig& cfg, std::ch
 
 }  // namespace
 
+ActorBehavior bulk_kernel_adapter(BatchKernel kernel) {
+  ActorBehavior behavior;
+  behavior.host_fire = [kernel = std::move(kernel)](HostFiringContext& ctx) {
+    std::vector<std::span<const std::byte>> inputs;
+    for (std::size_t i = 0; i < ctx.input_count(); ++i) inputs.push_back(ctx.input(i));
+    const std::vector<std::vector<std::byte>> produced = kernel(inputs);
+    if (produced.size() != ctx.output_count())
+      throw std::runtime_error("bulk kernel produced " + std::to_string(produced.size()) + " arrays for " +
+                               std::to_string(ctx.output_count()) + " ports");
+    for (std::size_t o = 0; o < produced.size(); ++o) {
+      const std::span<std::byte> region = ctx.output(o);
+      if (produced[o].size() != region.size())
+        throw std::runtime_error("bulk kernel output " + std::to_string(o) + " is " +
+                                 std::to_string(produced[o].size()) + " bytes, region is " +
+                                 std::to_string(region.size()));
+      std::memcpy(region.data(), produced[o].data(), region.size());
+    }
+  };
+  return behavior;
+}
+
 RunStats run(const NetworkGraph& net, const ExecutionConfig& cfg) {
   std::vector<Violation> violations = validate(net);
   if (!violations.empty()) {

@@ -51,6 +51,7 @@ def lib():
                                           C.POINTER(C.c_uint64)]
         L.dfh_read_cf32.argtypes = [C.c_char_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_uint64)]
         L.dfh_write_file.argtypes = [C.c_char_p, C.c_void_p, C.c_size_t]
+        L.dfh_bulk_kernel_run.argtypes = [C.c_int, C.c_uint32, C.c_uint64, C.c_int, C.c_void_p]
         L.dfh_synth.argtypes = [C.c_int, C.c_uint64, C.c_uint64, C.c_void_p]
         L.dfh_encode_config.argtypes = [C.c_uint16, C.c_void_p]
         L.dfh_decode_config.argtypes = [C.c_void_p, C.POINTER(C.c_uint16)]
@@ -257,4 +258,10 @@ def synth(what: str, n: int, seed: int) -> np.ndarray:
                           "samples": (2, np.float32, 2 * n), "frames": (3, np.uint8, n)}[what]
     out = np.empty(count, dtype)
     _check(lib().dfh_synth(kind, n, seed, out.ctypes.data_as(C.c_void_p)))
+    return out
+
+
+def bulk_kernel_run(rate: int, firings: int, bad: bool = False, device: int = 0) -> np.ndarray:
+    out = np.empty(firings * rate, np.int32)
+    _check(lib().dfh_bulk_kernel_run(device, rate, firings, int(bad), out.ctypes.data_as(C.c_void_p)))
     return out

@@ -144,3 +144,13 @@ def test_dynamic_cpu_actor_illegal_rate_is_actor_fault(gpu):
     with pytest.raises(H.HostRunError) as e:
         H.dynamic_cpu_run([3, 1, 9], 2, 6)
     assert "ActorFault" in str(e.value) and "control" in str(e.value)
+
+
+def test_bulk_kernel_adapter_cpu_actor(gpu):
+    # df::bulk_kernel_adapter (proj/include/dynflow/runtime.hpp:97-108): whole
+    # r-token regions to a batch kernel; a wrong output size faults the actor.
+    from paper_1611_03226_b200 import host_api as H
+    np.testing.assert_array_equal(H.bulk_kernel_run(5, 7), 2 * np.arange(35, dtype=np.int32))
+    with pytest.raises(H.HostRunError) as e:
+        H.bulk_kernel_run(5, 3, bad=True)
+    assert "ActorFault" in str(e.value) and "doubler" in str(e.value) and "region is 20" in str(e.value)
