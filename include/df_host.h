@@ -98,6 +98,10 @@ int dfh_dynamic_cpu_run(int device, const uint32_t* masks, size_t n_masks, uint3
  * faults the actor) -> sink.  out_host: firings * rate int32. */
 int dfh_bulk_kernel_run(int device, uint32_t rate, uint64_t firings, int bad, int32_t* out_host);
 
+/* df::Channel (include/df/channel.hpp, the reference's Channel API over a
+ * device channel): see host_abi.cpp for the scripted walk and status bits. */
+int dfh_channel_class_demo(int device, uint32_t rate, int delay, uint32_t firings, uint32_t* out, int* status);
+
 /* ---- data formats either side of the path (df/io.hpp, df/dpd.hpp) -------
  * The reference's text and file formats (proj/src/dpd.cpp:393-462
  * parse_schedule / parse_taps; proj/src/bench.cpp:25-97, :173-262 read_file

@@ -6,6 +6,7 @@
 
 #include <sstream>
 
+#include "df/channel.hpp"
 #include "df/dpd.hpp"
 #include "df/io.hpp"
 #include "df/motion.hpp"
@@ -484,6 +485,59 @@ int dfh_bulk_kernel_run(int device, uint32_t rate, uint64_t firings, int bad, in
     ec.device = device;
     ec.source_firing_limit = firings;
     run(build_network(actors, chans), ec);
+  });
+}
+
+// df::Channel (the reference's Channel API over a device channel): a host
+// producer writes `firings` regions of rate uint32 tokens (values 1, 2, ...),
+// a host consumer reads them back (a delay channel first yields its initial
+// token 0xFFFFFFFF); after close() the next read_start is end of stream.
+// out: firings * rate tokens read; status bits: 1 = end of stream seen,
+// 2 = write_start with n != rate threw logic_error, 4 = tokens_written and
+// tokens_read match, 8 = a read after abort() threw RunAborted.
+int dfh_channel_class_demo(int device, uint32_t rate, int delay, uint32_t firings, uint32_t* out, int* status) {
+  return guarded([&] {
+    using namespace df;
+    if (!out || !status) throw std::invalid_argument("dfh_channel_class_demo: null argument");
+    *status = 0;
+    std::vector<std::byte> init(4, std::byte{0xFF});
+    Channel ch({"c", 4, rate, delay != 0, delay ? init : std::vector<std::byte>{}}, device);
+    try {
+      ch.write_start(rate + 1);
+    } catch (const std::logic_error&) {
+      *status |= 2;
+    }
+    std::vector<std::uint32_t> v(rate);
+    std::uint32_t next = 1;
+    for (std::uint32_t f = 0; f < firings; ++f) {
+      RegionHandle w = ch.write_start(rate);
+      for (auto& x : v) x = next++;
+      check(df_memcpy_h2d(w.bytes.data(), v.data(), 4ull * rate, nullptr));
+      ch.write_end(w);
+      std::optional<RegionHandle> r = ch.read_start(rate);
+      if (!r) throw std::logic_error("unexpected end of stream");
+      check(df_memcpy_d2h(out + std::size_t(f) * rate, r->bytes.data(), 4ull * rate, nullptr));
+      ch.read_end(*r);
+    }
+    check(df_stream_synchronize(nullptr));
+    if (ch.tokens_written() == std::uint64_t(firings) * rate && ch.tokens_read() == std::uint64_t(firings) * rate)
+      *status |= 4;
+    ch.close();
+    for (int k = 0; k < 4; ++k) {  // drain what is left (a rate-1 delay channel still holds one token)
+      std::optional<RegionHandle> r = ch.read_start(rate);
+      if (!r) {
+        *status |= 1;
+        break;
+      }
+      ch.read_end(*r);
+    }
+    ch.abort();
+    try {
+      ch.read_start(rate);
+    } catch (const RunAborted&) {
+      *status |= 8;
+    }
+    ch.check_device();
   });
 }
 

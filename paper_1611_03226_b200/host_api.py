@@ -52,6 +52,8 @@ def lib():
         L.dfh_read_cf32.argtypes = [C.c_char_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_uint64)]
         L.dfh_write_file.argtypes = [C.c_char_p, C.c_void_p, C.c_size_t]
         L.dfh_bulk_kernel_run.argtypes = [C.c_int, C.c_uint32, C.c_uint64, C.c_int, C.c_void_p]
+        L.dfh_channel_class_demo.argtypes = [C.c_int, C.c_uint32, C.c_int, C.c_uint32, C.c_void_p,
+                                             C.POINTER(C.c_int)]
         L.dfh_synth.argtypes = [C.c_int, C.c_uint64, C.c_uint64, C.c_void_p]
         L.dfh_encode_config.argtypes = [C.c_uint16, C.c_void_p]
         L.dfh_decode_config.argtypes = [C.c_void_p, C.POINTER(C.c_uint16)]
@@ -265,3 +267,11 @@ def bulk_kernel_run(rate: int, firings: int, bad: bool = False, device: int = 0)
     out = np.empty(firings * rate, np.int32)
     _check(lib().dfh_bulk_kernel_run(device, rate, firings, int(bad), out.ctypes.data_as(C.c_void_p)))
     return out
+
+
+def channel_class_demo(rate: int, delay: bool, firings: int, device: int = 0):
+    out = np.empty(firings * rate, np.uint32)
+    st = C.c_int()
+    _check(lib().dfh_channel_class_demo(device, rate, int(delay), firings, out.ctypes.data_as(C.c_void_p),
+                                        C.byref(st)))
+    return out, st.value

@@ -150,3 +150,20 @@ def test_device_detects_overflow(gpu):
     s.synchronize()
     with pytest.raises(LogicError):
         ch.check()
+
+
+@pytest.mark.parametrize("rate", [1, 4])
+@pytest.mark.parametrize("delay", [False, True])
+def test_channel_class_api(gpu, rate, delay):
+    # df::Channel (include/df/channel.hpp): the reference's Channel calls over
+    # a device channel -- FIFO order (a delay channel first yields its initial
+    # token), n != rate -> logic_error, counters, end of stream after close,
+    # RunAborted after abort (proj/include/dynflow/channel.hpp:71-135).
+    from paper_1611_03226_b200 import host_api as H
+    firings = 5
+    out, status = H.channel_class_demo(rate, delay, firings)
+    stream = np.arange(1, firings * rate + 1, dtype=np.uint32)
+    if delay:  # the delay token shifts the stream by one token (Fig. 2)
+        stream = np.concatenate([[0xFFFFFFFF], stream[:-1]]).astype(np.uint32)
+    np.testing.assert_array_equal(out, stream)
+    assert status == 1 | 2 | 4 | 8, status
