@@ -162,10 +162,26 @@ __device__ __forceinline__ void hgauss4(unsigned L, unsigned C, unsigned R, unsi
 
 // Vertical [1 4 6 4 1] on 16x2 lanes (the +128 rides in the h bias);
 // max 16 * (4080 + 8) = 65408 < 2^16, so lanes never carry.
+// vgauss as four IMADs (FMA pipe) rather than IADD3/LEA (ALU pipe): the
+// motion kernels are issue-bound with the ALU pipe the busier one (ncu: ALU
+// 67 %, FMA 27 % of peak on 720p gray); moving the vertical gauss over gives
+// gray 720p -1.3 %, 4K RGB up to -4 % (profiles/r02_ab_motion_issue.txt).
+#ifndef DF_MOTION_VGAUSS_MAD
+#define DF_MOTION_VGAUSS_MAD 1
+#endif
+__device__ __forceinline__ unsigned mad_u32(unsigned a, unsigned b, unsigned c) {
+  unsigned d;  // a * b + c on the FMA pipe
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
 __device__ __forceinline__ unsigned vgauss(unsigned a, unsigned b, unsigned c, unsigned d,
                                           unsigned e) {
+#if DF_MOTION_VGAUSS_MAD
+  return mad_u32(c, 6u, mad_u32(mad_u32(b, 1u, d), 4u, mad_u32(a, 1u, e)));
+#else
   const unsigned B = b + d;
   return c * 6u + (B * 4u + (a + e));
+#endif
 }
 
 // |cur - prev| > thr per byte -> flag in bit 7 (other bits don't-care).
@@ -681,6 +697,13 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
 #ifndef DF_M3_TMA3D
 #define DF_M3_TMA3D 1
 #endif
+// fence.proxy.async before refilling a ring stage: not needed -- the stage's
+// shared-memory loads have all been consumed (their values used) before the
+// release, so no async-proxy write can overtake them (the CUTLASS consumer
+// release has no fence either).  Kept as an A/B switch.
+#ifndef DF_M3_PROXY_FENCE
+#define DF_M3_PROXY_FENCE 0
+#endif
 // 3-D tensor (column word, row, frame): rows outside [0, H) of a frame are
 // out of bounds and zero-filled without a DRAM read (a 2-D rows x frames
 // view would fetch the neighbouring frame's rows for the top and bottom
@@ -734,49 +757,73 @@ __device__ __forceinline__ void tmem_wait_ld(unsigned& a, unsigned& b) {
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // Per-warp row stream.  Group g = TMA box g = rows y0-3 + 5*(g % GPP) ..
-// +4 of pass g / GPP (pass P = frame fs + P), in ring stage g % kM3Stages,
-// completing its mbarrier phase (g / kM3Stages) & 1.  The 5-step unrolled
-// row loop consumes exactly one group per iteration, so a row's offset in
-// its box is a compile-time constant.
+// +4 of pass g / GPP (pass P = frame fs + dir*P, pass 0 of an inline-halo
+// stream = frame 0 of hmap), in ring stage g % kM3Stages, completing its
+// mbarrier phase (g / kM3Stages) & 1.  The 5-step unrolled row loop consumes
+// exactly one group per iteration, so a row's offset in its box is a
+// compile-time constant.  Groups are issued strictly in order, so the next
+// group's coordinates advance incrementally (no divisions, warp-uniform: every
+// lane advances them, lane 0 issues).
 template <int FMT, int R>
 struct M3Stream {
   static_assert(m3_valid_r<R>(), "band height");
   static constexpr int GPP = (R + 6) / kM3RPS;  // groups per frame pass
   const CUtensorMap* map;
-  const CUtensorMap* hmap;  // inline halo: pass 0 reads frame 0 of this map
-  bool hfirst;
   bool l2hint;        // L2 eviction hints on the band-halo rows (MotionGeom::l2hint)
   unsigned ring;      // smem address of this warp's ring
   unsigned bars;      // smem address of this warp's kM3Stages mbarriers
-  unsigned g;         // group being consumed
-  unsigned stage;     // g % kM3Stages
-  unsigned phase;     // (g / kM3Stages) & 1
-  unsigned groups;    // groups in the whole stream
+  unsigned stage;     // consumed group % kM3Stages
+  unsigned phase;     // (consumed group / kM3Stages) & 1
   unsigned cur;       // this lane's bytes in the current group's first row
   int c0;             // tensor column (uint32 units) of the warp tile
-  int fs, H, y0;
+  int H, y0;
   int dir;            // +1: pass P reads frame fs + P; -1: frame fs - P (backward chunk)
   int lane;
+  // Next group to issue.
+  int left;           // groups still to issue
+  unsigned nin;       // its index in its pass
+  int nrow;           // its first row
+  int nf, fnext;      // its frame; the frame of the pass after
+  const CUtensorMap* nmap;
 
-  __device__ __forceinline__ void issue(unsigned gi, unsigned s) {  // lane 0 only
-    if (gi >= groups) return;
-    const unsigned pass = gi / GPP;
-    int row = y0 - 3 + (int)(gi % GPP) * kM3RPS;
+  __device__ __forceinline__ void start(const CUtensorMap* m, const CUtensorMap* hm, bool hfirst, int fs,
+                                        unsigned passes) {
+    map = m;
+    left = (int)passes * GPP;
+    nin = 0;
+    nrow = y0 - 3;
+    nf = hfirst ? 0 : fs;
+    fnext = fs + dir;
+    nmap = hfirst ? hm : m;
+  }
+  // Lane 0: the TMA of the next group into stage s.
+  __device__ __forceinline__ void issue(unsigned s) const {
+    if (left <= 0) return;
     mbar_expect_tx(bars + 8 * s, kM3RPS * m3_row_bytes<FMT>());
-    const CUtensorMap* m = (hfirst && pass == 0) ? hmap : map;
 #if DF_M3_TMA3D
-    const int f = (hfirst && pass == 0) ? 0 : fs + dir * (int)pass;
+    const int row = nrow, f = nf;
 #else  // A/B baseline: frames stacked on the row axis (frame f at row f*H)
-    const int f = 0;
-    row += (hfirst && pass == 0) ? 0 : (fs + dir * (int)pass) * H;
+    const int row = nrow + (nmap == map ? nf * H : 0), f = 0;
 #endif
-    const unsigned in_pass = gi % GPP;
-    if (l2hint && in_pass < 2)
-      tma_load_3d_hint(ring + s * m3_stage_bytes<FMT>(), m, c0, row, f, bars + 8 * s, policy_evict_last());
-    else if (l2hint && in_pass == GPP - 1)
-      tma_load_3d_hint(ring + s * m3_stage_bytes<FMT>(), m, c0, row, f, bars + 8 * s, policy_evict_first());
+    const unsigned dst = ring + s * m3_stage_bytes<FMT>();
+    if (l2hint && nin < 2)
+      tma_load_3d_hint(dst, nmap, c0, row, f, bars + 8 * s, policy_evict_last());
+    else if (l2hint && nin == GPP - 1)
+      tma_load_3d_hint(dst, nmap, c0, row, f, bars + 8 * s, policy_evict_first());
     else
-      tma_load_3d(ring + s * m3_stage_bytes<FMT>(), m, c0, row, f, bars + 8 * s);
+      tma_load_3d(dst, nmap, c0, row, f, bars + 8 * s);
+  }
+  // Every lane: step the next-group state.
+  __device__ __forceinline__ void advance() {
+    --left;
+    nrow += kM3RPS;
+    if (++nin == GPP) {
+      nin = 0;
+      nrow = y0 - 3;
+      nf = fnext;
+      fnext += dir;
+      nmap = map;
+    }
   }
   __device__ __forceinline__ void acquire() {
     mbar_wait(bars + 8 * stage, phase);
@@ -788,10 +835,12 @@ struct M3Stream {
   __device__ __forceinline__ void release() {
     __syncwarp();
     if (lane == 0) {
+#if DF_M3_PROXY_FENCE
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(g + kM3Stages, stage);
+#endif
+      issue(stage);
     }
-    ++g;
+    advance();
     if (++stage == kM3Stages) {
       stage = 0;
       phase ^= 1;
@@ -965,7 +1014,7 @@ __device__ __forceinline__ void m3_pass(M3Stream<FMT, R>& st, unsigned char* __r
 }
 
 template <int FMT, int R, bool INT>
-__device__ __forceinline__ void m3_walk(M3Stream<FMT, R>& st, const unsigned char* prev_tok, unsigned char* out,
+__device__ __forceinline__ void m3_walk(M3Stream<FMT, R>& st, bool hfirst, const unsigned char* prev_tok, unsigned char* out,
                                         unsigned char* next_tok, unsigned char* next_copy, unsigned tmem, const MotionGeom& g, int y0, int x,
                                         int lane, int f_begin, int f_end) {
   const size_t frame_px = (size_t)g.W * g.H;
@@ -977,7 +1026,7 @@ __device__ __forceinline__ void m3_walk(M3Stream<FMT, R>& st, const unsigned cha
   // when it is the firing's last frame.
   if (st.dir < 0 && f_end == g.frames) {
     m3_pass<FMT, R, 3, INT>(st, nullptr, next_tok, next_copy, tmem, g, y0, x, lane, gm, mm);
-  } else if (st.dir > 0 && f_begin == 0 && !st.hfirst) {
+  } else if (st.dir > 0 && f_begin == 0 && !hfirst) {
     // Delay token: gauss of the previous firing's last frame -> TMEM.
     for (int r = 0; r < R + 2; ++r) {
       unsigned a0 = 0u, a1 = 0u;  // null token: black (proj/src/motion.cpp:131)
@@ -1037,14 +1086,11 @@ __global__ void __launch_bounds__(32 * kM3Warps, DF_M3_MINB) motion_m3_kernel(co
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   M3Stream<FMT, R> st;
-  st.map = &map;
-  st.hmap = &hmap;
   // Inline halo (raw mode): the first chunk warms up on the halo frame
   // instead of loading a delay token -- gauss(halo) never goes through HBM.
-  st.hfirst = io.halo != nullptr && f_begin == 0;
+  const bool hfirst = io.halo != nullptr && f_begin == 0;
   st.ring = smem_u32(m3_smem + warp * m3_ring_bytes<FMT>());
   st.bars = smem_u32(m3_smem + kM3Warps * m3_ring_bytes<FMT>() + warp * kM3Stages * 8);
-  st.g = 0;
   st.stage = 0;
   st.phase = 0;
   st.cur = 0;
@@ -1082,10 +1128,9 @@ __global__ void __launch_bounds__(32 * kM3Warps, DF_M3_MINB) motion_m3_kernel(co
   // inline halo) always walks forward.
   const bool back = DF_M3_ALT && (chunk & 1) && f_begin < f_end;
   st.dir = back ? -1 : 1;
-  const int f_first = back ? f_end - 1 : (f_begin > 0 || st.hfirst) ? f_begin - 1 : f_begin;  // first frame read
-  st.fs = base + f_first;
+  const int f_first = back ? f_end - 1 : (f_begin > 0 || hfirst) ? f_begin - 1 : f_begin;  // first frame read
   const int passes = f_begin >= f_end ? 0 : back ? f_end - f_begin + 1 : f_end - f_first;
-  st.groups = (unsigned)passes * M3Stream<FMT, R>::GPP;
+  st.start(&map, &hmap, hfirst, base + f_first, (unsigned)passes);
   if (lane == 0) {
     for (int s = 0; s < kM3Stages; ++s) mbar_init(st.bars + 8 * s, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1099,13 +1144,15 @@ __global__ void __launch_bounds__(32 * kM3Warps, DF_M3_MINB) motion_m3_kernel(co
                         (unsigned)((warp >> 2) * m3_warp_cols<R>());
 
   if (passes > 0) {
-    if (lane == 0)
-      for (int s = 0; s < kM3Stages; ++s) st.issue(s, s);
+    for (int s = 0; s < kM3Stages; ++s) {
+      if (lane == 0) st.issue(s);
+      st.advance();
+    }
     const bool interior = y0 >= 3 && y0 + R <= g.H - 3;  // no border gauss/median row
     if (interior)
-      m3_walk<FMT, R, true>(st, prev_tok, out, next_tok, next_copy, tmem, g, y0, x, lane, f_begin, f_end);
+      m3_walk<FMT, R, true>(st, hfirst, prev_tok, out, next_tok, next_copy, tmem, g, y0, x, lane, f_begin, f_end);
     else
-      m3_walk<FMT, R, false>(st, prev_tok, out, next_tok, next_copy, tmem, g, y0, x, lane, f_begin, f_end);
+      m3_walk<FMT, R, false>(st, hfirst, prev_tok, out, next_tok, next_copy, tmem, g, y0, x, lane, f_begin, f_end);
   }
   tmem_wait_st();
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
