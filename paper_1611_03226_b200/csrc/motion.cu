@@ -162,10 +162,7 @@ __device__ __forceinline__ void hgauss4(unsigned L, unsigned C, unsigned R, unsi
 
 // Vertical [1 4 6 4 1] on 16x2 lanes (the +128 rides in the h bias);
 // max 16 * (4080 + 8) = 65408 < 2^16, so lanes never carry.
-// vgauss as four IMADs (FMA pipe) rather than IADD3/LEA (ALU pipe): the
-// motion kernels are issue-bound with the ALU pipe the busier one (ncu: ALU
-// 67 %, FMA 27 % of peak on 720p gray); moving the vertical gauss over gives
-// gray 720p -1.3 %, 4K RGB up to -4 % (profiles/r02_ab_motion_issue.txt).
+// M3's vertical gauss written as mad.lo (see vgauss_fma).
 #ifndef DF_MOTION_VGAUSS_MAD
 #define DF_MOTION_VGAUSS_MAD 1
 #endif
@@ -176,11 +173,18 @@ __device__ __forceinline__ unsigned mad_u32(unsigned a, unsigned b, unsigned c) 
 }
 __device__ __forceinline__ unsigned vgauss(unsigned a, unsigned b, unsigned c, unsigned d,
                                           unsigned e) {
+  const unsigned B = b + d;
+  return c * 6u + (B * 4u + (a + e));
+}
+// The same sum written as four mad.lo (M3).  ptxas keeps some as IMAD (FMA
+// pipe) and turns others into IADD3/LEA; this mix measured faster than both
+// the plain form and all-IMAD (multipliers from the constant bank, which
+// ptxas cannot strength-reduce): profiles/r02_ab_motion_issue.txt.
+__device__ __forceinline__ unsigned vgauss_fma(unsigned a, unsigned b, unsigned c, unsigned d, unsigned e) {
 #if DF_MOTION_VGAUSS_MAD
   return mad_u32(c, 6u, mad_u32(mad_u32(b, 1u, d), 4u, mad_u32(a, 1u, e)));
 #else
-  const unsigned B = b + d;
-  return c * 6u + (B * 4u + (a + e));
+  return vgauss(a, b, c, d, e);
 #endif
 }
 
@@ -319,9 +323,10 @@ __device__ __forceinline__ void store_bytes8(unsigned char* __restrict__ plane, 
 
 // Byte masks (0xFF per byte) of columns in the gauss border (x < 2 or
 // x >= W-2) and the median border (x == 0 or x == W-1).
-__device__ __forceinline__ void column_masks(int x, int W, unsigned gm[2], unsigned mm[2]) {
+template <int WPL = 2>
+__device__ __forceinline__ void column_masks(int x, int W, unsigned gm[WPL], unsigned mm[WPL]) {
 #pragma unroll
-  for (int w = 0; w < 2; ++w) {
+  for (int w = 0; w < WPL; ++w) {
     unsigned a = 0, b = 0;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -645,35 +650,57 @@ constexpr size_t kSmemBytes = sizeof(uint2) * kWarpsPerCta * (kBandRows + 2) * 3
 #define DF_M3_PDL 1  // programmatic dependent launch (setup overlaps the previous kernel's tail)
 #endif
 constexpr int kM3Warps = DF_M3_WARPS;
+// Gray input: 16 px per lane (4 gray words) in 12-warp CTAs.  The kernel is
+// issue-bound on gray, and the per-row per-lane fixed work (row load, the 4
+// neighbour shuffles, TMEM load/store, output store, loop control, ring
+// refill) is then shared by 16 px instead of 8; 12 warps x 4(R + 2) TMEM
+// columns keep R = 39.  RGB keeps 8 px per lane (its 24 B/lane/row and
+// RGB->gray registers) in 20-warp CTAs.
+#ifndef DF_M3_GRAY_PX
+#define DF_M3_GRAY_PX 16
+#endif
+#ifndef DF_M3_WIDE_WARPS
+#define DF_M3_WIDE_WARPS 12
+#endif
+template <int FMT>
+struct M3Cfg {
+  static constexpr int PX = FMT == DF_MOTION_GRAY ? DF_M3_GRAY_PX : kPxPerLane;  // px per lane
+  static constexpr int WPL = PX / 4;                                            // gray words per lane
+  static constexpr int NW = PX == 16 ? DF_M3_WIDE_WARPS : kM3Warps;             // warps per CTA
+  static constexpr int OUT = 30 * PX;                                           // output px per warp tile
+  // A TMA box's innermost start must be 16-byte aligned.  Tile rows start at
+  // FMT * (OUT t - PX) bytes: 8 bytes past a 16-byte boundary for PX = 8
+  // (3 * (240 t - 8) = 720 t - 24 RGB, 240 t - 8 gray), so each box row is
+  // the tile row plus 8 bytes on both sides; aligned for gray PX = 16.
+  static constexpr int LEAD = (PX * FMT) % 16 == 0 ? 0 : 8;
+  static constexpr int BPL = PX * FMT;  // input bytes per lane per row
+};
+static_assert(DF_M3_GRAY_PX == 8 || DF_M3_GRAY_PX == 16, "gray px per lane");
 // Band heights R (template parameter): a frame pass fetches rows y0-3 ..
 // y0+R+2 (R + 6 rows, whole 5-row boxes), gauss(prev) holds R + 2 rows in
-// 2(R + 2) <= 128 TMEM columns.  launch_m3 picks R per frame geometry.
+// WPL(R + 2) TMEM columns per warp.  launch_m3 picks R per frame geometry.
 constexpr int kTmemCols = kM3Warps > 4 ? 512 : 128;
-template <int R>
-constexpr int m3_warp_cols() { return 2 * (R + 2); }
-template <int R>
+template <int FMT, int R>
+constexpr int m3_warp_cols() { return M3Cfg<FMT>::WPL * (R + 2); }
+template <int FMT, int R>
 constexpr bool m3_valid_r() {
-  return (R + 6) % 5 == 0 && m3_warp_cols<R>() * ((kM3Warps + 3) / 4) <= kTmemCols;
+  return (R + 6) % 5 == 0 && m3_warp_cols<FMT, R>() * ((M3Cfg<FMT>::NW + 3) / 4) <= kTmemCols;
 }
 constexpr int kM3RPS = DF_M3_RPS;
 constexpr int kM3Stages = DF_M3_ST;
 static_assert(kM3RPS == 5, "one TMA box per 5-step iteration of the row loop (static in-box row offsets)");
 
-// A TMA box's innermost start must be 16-byte aligned, and a warp tile's
-// row starts 8 bytes past a 16-byte boundary (3 * (240 t - 8) = 720 t - 24
-// RGB, 240 t - 8 gray): each box row is the tile row plus 8 bytes on both
-// sides, and lane l's bytes sit at offset 8 + 8*FMT*l.
 template <int FMT>
-constexpr int m3_row_bytes() { return 32 * kPxPerLane * FMT + 16; }  // 784 / 272 B
+constexpr int m3_row_bytes() { return 32 * M3Cfg<FMT>::BPL + 2 * M3Cfg<FMT>::LEAD; }  // 784 RGB / 512 gray B
 template <int FMT>
 constexpr int m3_stage_bytes() { return (kM3RPS * m3_row_bytes<FMT>() + 127) / 128 * 128; }
-// Dynamic smem: kM3Warps rings (128-B aligned stages for TMA), then the
+// Dynamic smem: NW rings (128-B aligned stages for TMA), then the
 // mbarriers, then the TMEM base address slot.
 template <int FMT>
 constexpr size_t m3_ring_bytes() { return (size_t)kM3Stages * m3_stage_bytes<FMT>(); }
 template <int FMT>
 constexpr size_t m3_smem_bytes() {
-  return kM3Warps * m3_ring_bytes<FMT>() + kM3Warps * kM3Stages * 8 + 16;
+  return M3Cfg<FMT>::NW * m3_ring_bytes<FMT>() + M3Cfg<FMT>::NW * kM3Stages * 8 + 16;
 }
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -755,6 +782,36 @@ __device__ __forceinline__ void tmem_wait_ld(unsigned& a, unsigned& b) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(a), "+r"(b)::"memory");
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_st4(unsigned taddr, const unsigned (&v)[4]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr), "r"(v[0]), "r"(v[1]),
+               "r"(v[2]), "r"(v[3])
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld4(unsigned taddr, unsigned (&v)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+               : "r"(taddr)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld4(unsigned (&v)[4]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3])::"memory");
+}
+// One gauss row of a lane (N = 2 or 4 words) to / from TMEM.
+template <int N>
+__device__ __forceinline__ void tmem_st_row(unsigned taddr, const unsigned (&v)[N]) {
+  if constexpr (N == 2) tmem_st2(taddr, v[0], v[1]);
+  else tmem_st4(taddr, v);
+}
+template <int N>
+__device__ __forceinline__ void tmem_ld_row(unsigned taddr, unsigned (&v)[N]) {
+  if constexpr (N == 2) tmem_ld2(taddr, v[0], v[1]);
+  else tmem_ld4(taddr, v);
+}
+template <int N>
+__device__ __forceinline__ void tmem_wait_row(unsigned (&v)[N]) {
+  if constexpr (N == 2) tmem_wait_ld(v[0], v[1]);
+  else tmem_wait_ld4(v);
+}
 
 // Per-warp row stream.  Group g = TMA box g = rows y0-3 + 5*(g % GPP) ..
 // +4 of pass g / GPP (pass P = frame fs + dir*P, pass 0 of an inline-halo
@@ -766,7 +823,7 @@ __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.
 // lane advances them, lane 0 issues).
 template <int FMT, int R>
 struct M3Stream {
-  static_assert(m3_valid_r<R>(), "band height");
+  static_assert(m3_valid_r<FMT, R>(), "band height");
   static constexpr int GPP = (R + 6) / kM3RPS;  // groups per frame pass
   const CUtensorMap* map;
   bool l2hint;        // L2 eviction hints on the band-halo rows (MotionGeom::l2hint)
@@ -827,7 +884,7 @@ struct M3Stream {
   }
   __device__ __forceinline__ void acquire() {
     mbar_wait(bars + 8 * stage, phase);
-    cur = ring + stage * m3_stage_bytes<FMT>() + 8 + lane * (kPxPerLane * FMT);
+    cur = ring + stage * m3_stage_bytes<FMT>() + M3Cfg<FMT>::LEAD + lane * M3Cfg<FMT>::BPL;
   }
   __device__ __forceinline__ unsigned row(int k) const { return cur + k * m3_row_bytes<FMT>(); }
   // After the group's bytes are in registers (and used): refill its stage
@@ -854,11 +911,25 @@ __device__ __forceinline__ uint2 lds64(unsigned a) {
   return v;
 }
 
+__device__ __forceinline__ uint4 lds128(unsigned a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+
+template <int WPL>
 struct M3Row {
-  unsigned h[4];  // horizontal sums, 16x2 packed
-  unsigned g[2];  // gray words
-  unsigned t[2];  // threshold flags
+  unsigned h[2 * WPL];  // horizontal sums, 16x2 packed
+  unsigned g[WPL];      // gray words
+  unsigned t[WPL];      // threshold flags
 };
+
+// WPL words (4 px each) of a lane to global memory (8 or 16 bytes).
+template <int WPL>
+__device__ __forceinline__ void store_words(unsigned char* p, const unsigned (&v)[WPL]) {
+  if constexpr (WPL == 2) *reinterpret_cast<uint2*>(p) = make_uint2(v[0], v[1]);
+  else *reinterpret_cast<uint4*>(p) = make_uint4(v[0], v[1], v[2], v[3]);
+}
 
 // One frame pass (MODE 0 warm-up / 1 chain / 2 chain + delay token / 3
 // warm-up + delay token) of the warp's (tile, band).  INT: interior band (no
@@ -867,10 +938,13 @@ template <int FMT, int R, int MODE, bool INT>
 __device__ __forceinline__ void m3_pass(M3Stream<FMT, R>& st, unsigned char* __restrict__ out,
                                         unsigned char* __restrict__ next_tok, unsigned char* __restrict__ next_copy,
                                         unsigned tmem, const MotionGeom& g,
-                                        int y0, int x, int lane, const unsigned gm[2], const unsigned mm[2]) {
+                                        int y0, int x, int lane, const unsigned (&gm)[M3Cfg<FMT>::WPL],
+                                        const unsigned (&mm)[M3Cfg<FMT>::WPL]) {
+  constexpr int WPL = M3Cfg<FMT>::WPL;
+  constexpr int NIN = M3Cfg<FMT>::BPL / 4;  // input words per lane per row
   const int W = g.W, H = g.H;
   const bool out_lane = lane >= 1 && lane <= 30;
-  M3Row s[5];
+  M3Row<WPL> s[5];
   unsigned ooff = (unsigned)y0 * (unsigned)W + (unsigned)x;
   // Each prev row is read (tcgen05.ld, waited) before it is overwritten in
   // the same step; the previous pass's stores must have landed before this
@@ -883,84 +957,93 @@ __device__ __forceinline__ void m3_pass(M3Stream<FMT, R>& st, unsigned char* __r
   // released at k == 4.  fetch() reads the row's words from the ring;
   // finish() converts them (split so a step can issue its shared-memory
   // loads before the gauss/thres/median work that hides their latency).
-  auto fetch = [&](int k, uint2 (&w)[3]) {
+  auto fetch = [&](int k, unsigned (&w)[NIN]) {
     if (k == 0) st.acquire();
     const unsigned a = st.row(k);
-    w[0] = lds64(a);
-    if (FMT == DF_MOTION_RGB) {
-      w[1] = lds64(a + 8);
-      w[2] = lds64(a + 16);
+    if constexpr (NIN == 4) {
+      const uint4 v = lds128(a);
+      w[0] = v.x, w[1] = v.y, w[2] = v.z, w[3] = v.w;
+    } else {
+#pragma unroll
+      for (int i = 0; i < NIN / 2; ++i) {
+        const uint2 v = lds64(a + 8 * i);
+        w[2 * i] = v.x, w[2 * i + 1] = v.y;
+      }
     }
   };
-  auto finish = [&](M3Row& r, int k, const uint2 (&w)[3]) {
-    unsigned g0, g1;
-    if (FMT == DF_MOTION_RGB) {
-      g0 = rgb4_to_gray(w[0].x, w[0].y, w[1].x, g.wg);
-      g1 = rgb4_to_gray(w[1].y, w[2].x, w[2].y, g.wg);
+  auto finish = [&](M3Row<WPL>& r, int k, const unsigned (&w)[NIN]) {
+    unsigned gw[WPL];
+    if constexpr (FMT == DF_MOTION_RGB) {
+      gw[0] = rgb4_to_gray(w[0], w[1], w[2], g.wg);
+      gw[1] = rgb4_to_gray(w[3], w[4], w[5], g.wg);
     } else {
-      g0 = w[0].x;
-      g1 = w[0].y;
+#pragma unroll
+      for (int i = 0; i < WPL; ++i) gw[i] = w[i];
     }
-    const unsigned left = __shfl_up_sync(0xffffffffu, g1, 1);
-    const unsigned right = __shfl_down_sync(0xffffffffu, g0, 1);
-    hgauss4(left, g0, g1, r.h[0], r.h[1], g.wh);
-    hgauss4(g0, g1, right, r.h[2], r.h[3], g.wh);
-    r.g[0] = g0;
-    r.g[1] = g1;
+    const unsigned left = __shfl_up_sync(0xffffffffu, gw[WPL - 1], 1);
+    const unsigned right = __shfl_down_sync(0xffffffffu, gw[0], 1);
+#pragma unroll
+    for (int i = 0; i < WPL; ++i)
+      hgauss4(i == 0 ? left : gw[i - 1], gw[i], i == WPL - 1 ? right : gw[i + 1], r.h[2 * i], r.h[2 * i + 1], g.wh);
+#pragma unroll
+    for (int i = 0; i < WPL; ++i) r.g[i] = gw[i];
     if (k == kM3RPS - 1) st.release();
   };
-  auto produce = [&](M3Row& r, int k) {
-    uint2 w[3];
+  auto produce = [&](M3Row<WPL>& r, int k) {
+    unsigned w[NIN];
     fetch(k, w);
     finish(r, k, w);
   };
 
-  auto gauss_thres = [&](M3Row& r4, M3Row& r3, M3Row& r2, M3Row& r1, M3Row& r0, int gc) {
-    const unsigned ta = tmem + 2u * (unsigned)(gc - (y0 - 1));
-    unsigned p0 = 0, p1 = 0;
-    if (CHAIN) tmem_ld2(ta, p0, p1);
-    unsigned gw[2];
+  auto gauss_thres = [&](M3Row<WPL>& r4, M3Row<WPL>& r3, M3Row<WPL>& r2, M3Row<WPL>& r1, M3Row<WPL>& r0, int gc) {
+    const unsigned ta = tmem + (unsigned)WPL * (unsigned)(gc - (y0 - 1));
+    unsigned p[WPL];
+    if (CHAIN) tmem_ld_row<WPL>(ta, p);
+    unsigned gw[WPL];
     if (!INT && (unsigned)(gc - 2) >= (unsigned)(H - 4)) {  // gc < 2 || gc >= H-2: gray copied
-      gw[0] = r2.g[0];
-      gw[1] = r2.g[1];
+#pragma unroll
+      for (int w = 0; w < WPL; ++w) gw[w] = r2.g[w];
     } else {
 #pragma unroll
-      for (int w = 0; w < 2; ++w) {
-        const unsigned v0 = vgauss(r4.h[2 * w], r3.h[2 * w], r2.h[2 * w], r1.h[2 * w], r0.h[2 * w]);
+      for (int w = 0; w < WPL; ++w) {
+        const unsigned v0 = vgauss_fma(r4.h[2 * w], r3.h[2 * w], r2.h[2 * w], r1.h[2 * w], r0.h[2 * w]);
         const unsigned v1 =
-            vgauss(r4.h[2 * w + 1], r3.h[2 * w + 1], r2.h[2 * w + 1], r1.h[2 * w + 1], r0.h[2 * w + 1]);
+            vgauss_fma(r4.h[2 * w + 1], r3.h[2 * w + 1], r2.h[2 * w + 1], r1.h[2 * w + 1], r0.h[2 * w + 1]);
         gw[w] = lop_sel(gm[w], r2.g[w], prmt(v0, v1, 0x7531));
       }
     }
     if (CHAIN) {
-      tmem_wait_ld(p0, p1);
-      r2.t[0] = thres4(gw[0], p0, g);
-      r2.t[1] = thres4(gw[1], p1, g);
+      tmem_wait_row<WPL>(p);
+#pragma unroll
+      for (int w = 0; w < WPL; ++w) r2.t[w] = thres4(gw[w], p[w], g);
     }
-    tmem_st2(ta, gw[0], gw[1]);
+    tmem_st_row<WPL>(ta, gw);
     if (TOK && out_lane && x < W && gc >= y0 && gc < y0 + R && gc < H) {
       const unsigned o = (unsigned)gc * (unsigned)W + (unsigned)x;
-      *reinterpret_cast<uint2*>(next_tok + o) = make_uint2(gw[0], gw[1]);
-      if (next_copy) *reinterpret_cast<uint2*>(next_copy + o) = make_uint2(gw[0], gw[1]);  // Fig. 2 phase 2
+      store_words<WPL>(next_tok + o, gw);
+      if (next_copy) store_words<WPL>(next_copy + o, gw);  // Fig. 2 phase 2
     }
   };
 
-  auto median = [&](M3Row& r4, M3Row& r3, M3Row& r2, int m) {
-    const unsigned c0 = r3.t[0], c1 = r3.t[1];
-    const unsigned lnb = __shfl_up_sync(0xffffffffu, c1, 1);
-    const unsigned rnb = __shfl_down_sync(0xffffffffu, c0, 1);
-    unsigned o0, o1;
+  auto median = [&](M3Row<WPL>& r4, M3Row<WPL>& r3, M3Row<WPL>& r2, int m) {
+    const unsigned lnb = __shfl_up_sync(0xffffffffu, r3.t[WPL - 1], 1);
+    const unsigned rnb = __shfl_down_sync(0xffffffffu, r3.t[0], 1);
+    unsigned o[WPL];
     if (!INT && (unsigned)(m - 1) >= (unsigned)(H - 2)) {  // m == 0 || m == H-1: copied
-      o0 = c0;
-      o1 = c1;
+#pragma unroll
+      for (int w = 0; w < WPL; ++w) o[w] = r3.t[w];
     } else {
-      const unsigned l0 = __funnelshift_l(lnb, c0, 8), r0w = __funnelshift_r(c0, c1, 8);
-      const unsigned l1 = __funnelshift_l(c0, c1, 8), r1w = __funnelshift_r(c1, rnb, 8);
-      o0 = lop_sel(mm[0], c0, maj5(c0, r4.t[0], r2.t[0], l0, r0w));
-      o1 = lop_sel(mm[1], c1, maj5(c1, r4.t[1], r2.t[1], l1, r1w));
+#pragma unroll
+      for (int w = 0; w < WPL; ++w) {
+        const unsigned c = r3.t[w];
+        const unsigned l = __funnelshift_l(w == 0 ? lnb : r3.t[w - 1], c, 8);
+        const unsigned rw = __funnelshift_r(c, w == WPL - 1 ? rnb : r3.t[w + 1], 8);
+        o[w] = lop_sel(mm[w], c, maj5(c, r4.t[w], r2.t[w], l, rw));
+      }
     }
-    if (out_lane && x < W)
-      *reinterpret_cast<uint2*>(out + ooff) = make_uint2(prmt(o0, 0, 0xBA98), prmt(o1, 0, 0xBA98));
+#pragma unroll
+    for (int w = 0; w < WPL; ++w) o[w] = prmt(o[w], 0, 0xBA98);
+    if (out_lane && x < W) store_words<WPL>(out + ooff, o);
     ooff += (unsigned)W;
   };
 
@@ -968,9 +1051,9 @@ __device__ __forceinline__ void m3_pass(M3Stream<FMT, R>& st, unsigned char* __r
   // Step gc produces row gc+3 = stream row gc - y0 + 6 of the pass: in-group
   // position (gc - y0 + 1) % 5, i.e. the step's position k in the unrolled
   // 5-step body (the body starts at gc = y0 - 1 + 5i).
-  auto step = [&](M3Row& r4, M3Row& r3, M3Row& r2, M3Row& r1, M3Row& r0, int gc, int k) {
+  auto step = [&](M3Row<WPL>& r4, M3Row<WPL>& r3, M3Row<WPL>& r2, M3Row<WPL>& r1, M3Row<WPL>& r0, int gc, int k) {
     if constexpr (R >= DF_M3_EARLY_MIN_R) {
-      uint2 w[3] = {};
+      unsigned w[NIN] = {};
       if (gc < gc_end) fetch(k, w);
       gauss_thres(r4, r3, r2, r1, r0, gc);
       if (CHAIN && gc > y0) median(r4, r3, r2, gc - 1);
@@ -1017,9 +1100,10 @@ template <int FMT, int R, bool INT>
 __device__ __forceinline__ void m3_walk(M3Stream<FMT, R>& st, bool hfirst, const unsigned char* prev_tok, unsigned char* out,
                                         unsigned char* next_tok, unsigned char* next_copy, unsigned tmem, const MotionGeom& g, int y0, int x,
                                         int lane, int f_begin, int f_end) {
+  constexpr int WPL = M3Cfg<FMT>::WPL;
   const size_t frame_px = (size_t)g.W * g.H;
-  unsigned gm[2], mm[2];
-  column_masks(x, g.W, gm, mm);
+  unsigned gm[WPL], mm[WPL];
+  column_masks<WPL>(x, g.W, gm, mm);
   // First pass: gauss of the frame before the chunk's first output (forward)
   // or of its last frame (backward, see motion_m3_kernel) into TMEM -- or
   // the delay token.  A backward chunk's first gauss is the next delay token
@@ -1029,9 +1113,12 @@ __device__ __forceinline__ void m3_walk(M3Stream<FMT, R>& st, bool hfirst, const
   } else if (st.dir > 0 && f_begin == 0 && !hfirst) {
     // Delay token: gauss of the previous firing's last frame -> TMEM.
     for (int r = 0; r < R + 2; ++r) {
-      unsigned a0 = 0u, a1 = 0u;  // null token: black (proj/src/motion.cpp:131)
-      if (prev_tok) load_bytes8<true>(prev_tok, y0 - 1 + r, x, g.W, g.H, a0, a1);
-      tmem_st2(tmem + 2u * r, a0, a1);
+      unsigned v[WPL] = {};  // null token: black (proj/src/motion.cpp:131)
+      if (prev_tok)
+#pragma unroll
+        for (int i = 0; i < WPL / 2; ++i)
+          load_bytes8<true>(prev_tok, y0 - 1 + r, x + 8 * i, g.W, g.H, v[2 * i], v[2 * i + 1]);
+      tmem_st_row<WPL>(tmem + (unsigned)(WPL * r), v);
     }
   } else {  // gauss of the first frame read: f_begin - 1 (or the inline halo frame), or f_end - 1
     m3_pass<FMT, R, 0, INT>(st, nullptr, nullptr, nullptr, tmem, g, y0, x, lane, gm, mm);
@@ -1050,7 +1137,7 @@ __device__ __forceinline__ void m3_walk(M3Stream<FMT, R>& st, bool hfirst, const
 }
 
 template <int FMT, int R>
-__global__ void __launch_bounds__(32 * kM3Warps, DF_M3_MINB) motion_m3_kernel(const __grid_constant__ CUtensorMap map,
+__global__ void __launch_bounds__(32 * M3Cfg<FMT>::NW, DF_M3_MINB) motion_m3_kernel(const __grid_constant__ CUtensorMap map,
                                                                    const __grid_constant__ CUtensorMap hmap,
                                                                    MotionIO io, MotionGeom g,
                                                                    unsigned* done_counter) {
@@ -1061,13 +1148,14 @@ __global__ void __launch_bounds__(32 * kM3Warps, DF_M3_MINB) motion_m3_kernel(co
   const int lane = threadIdx.x & 31, warp = __shfl_sync(0xffffffffu, (int)threadIdx.x >> 5, 0);
   // Warp task t (1-D grid): consecutive tasks are consecutive temporal chunks
   // of one (tile, band), so a 4-warp CTA holds 4 chunks of one band as before.
-  const int task = (int)blockIdx.x * kM3Warps + warp;
+  using Cfg = M3Cfg<FMT>;
+  const int task = (int)blockIdx.x * Cfg::NW + warp;
   const int chunk = task % g.m3_chunks;
   const int band = (task / g.m3_chunks) % g.m3_bands;
   const int tile = task / (g.m3_chunks * g.m3_bands);
   const int y0 = band * R;
-  const int tx0 = tile * kOutPxPerWarp - kPxPerLane;
-  const int x = tx0 + lane * kPxPerLane;
+  const int tx0 = tile * Cfg::OUT - Cfg::PX;
+  const int x = tx0 + lane * Cfg::PX;
   const int f_begin = chunk * g.chunk;
   // Tasks past the last tile (the grid's last CTA) walk no frames.
   const int f_end = tx0 < g.W ? min(f_begin + g.chunk, g.frames) : f_begin;
@@ -1078,7 +1166,7 @@ __global__ void __launch_bounds__(32 * kM3Warps, DF_M3_MINB) motion_m3_kernel(co
   // waits for the previous grid before touching anything it produced.
   asm volatile("griddepcontrol.launch_dependents;");
 #endif
-  unsigned* tmem_slot = reinterpret_cast<unsigned*>(m3_smem + kM3Warps * m3_ring_bytes<FMT>() + kM3Warps * kM3Stages * 8);
+  unsigned* tmem_slot = reinterpret_cast<unsigned*>(m3_smem + Cfg::NW * m3_ring_bytes<FMT>() + Cfg::NW * kM3Stages * 8);
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "n"(kTmemCols)
@@ -1090,11 +1178,11 @@ __global__ void __launch_bounds__(32 * kM3Warps, DF_M3_MINB) motion_m3_kernel(co
   // instead of loading a delay token -- gauss(halo) never goes through HBM.
   const bool hfirst = io.halo != nullptr && f_begin == 0;
   st.ring = smem_u32(m3_smem + warp * m3_ring_bytes<FMT>());
-  st.bars = smem_u32(m3_smem + kM3Warps * m3_ring_bytes<FMT>() + warp * kM3Stages * 8);
+  st.bars = smem_u32(m3_smem + Cfg::NW * m3_ring_bytes<FMT>() + warp * kM3Stages * 8);
   st.stage = 0;
   st.phase = 0;
   st.cur = 0;
-  st.c0 = (tx0 * FMT - 8) / 4;  // 16-byte aligned box start (see m3_row_bytes)
+  st.c0 = (tx0 * FMT - Cfg::LEAD) / 4;  // 16-byte aligned box start (see M3Cfg::LEAD)
   st.l2hint = g.l2hint;
   st.H = g.H;
   st.y0 = y0;
@@ -1141,7 +1229,7 @@ __global__ void __launch_bounds__(32 * kM3Warps, DF_M3_MINB) motion_m3_kernel(co
   // Lane quarter warp % 4 (a warp may only access its own quarter), column
   // block warp / 4.
   const unsigned tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0) + ((unsigned)(32 * (warp & 3)) << 16) +
-                        (unsigned)((warp >> 2) * m3_warp_cols<R>());
+                        (unsigned)((warp >> 2) * m3_warp_cols<FMT, R>());
 
   if (passes > 0) {
     for (int s = 0; s < kM3Stages; ++s) {
@@ -1332,12 +1420,21 @@ constexpr int kM3Heights[3] = {39, 44, 49};  // 5 warps per lane quarter: 2(R + 
 #else
 constexpr int kM3Heights[3] = {49, 54, 59};
 #endif
+#if DF_M3_WIDE_WARPS > 12
+constexpr int kM3WideHeights[3] = {19, 24, 29};  // 16 px per lane, 4 warps per lane quarter: 4(R + 2) <= 128
+#else
+constexpr int kM3WideHeights[3] = {29, 34, 39};  // 16 px per lane, 3 warps per lane quarter: 4(R + 2) <= 170
+#endif
+template <int FMT>
+constexpr int m3_height(int ri) {
+  return M3Cfg<FMT>::PX == 16 ? kM3WideHeights[ri] : kM3Heights[ri];
+}
 
 template <int FMT>
 const void* m3_kernel_fn(int ri) {
-  return ri == 0 ? (const void*)motion_m3_kernel<FMT, kM3Heights[0]>
-                 : ri == 1 ? (const void*)motion_m3_kernel<FMT, kM3Heights[1]>
-                           : (const void*)motion_m3_kernel<FMT, kM3Heights[2]>;
+  return ri == 0 ? (const void*)motion_m3_kernel<FMT, m3_height<FMT>(0)>
+                 : ri == 1 ? (const void*)motion_m3_kernel<FMT, m3_height<FMT>(1)>
+                           : (const void*)motion_m3_kernel<FMT, m3_height<FMT>(2)>;
 }
 
 struct M3Plan {
@@ -1345,9 +1442,11 @@ struct M3Plan {
   double cost;
 };
 
+template <int FMT>
 M3Plan m3_plan(const df_motion* m, int frames, int ri) {
-  const int R = kM3Heights[ri];
-  const int tiles = (m->W + kOutPxPerWarp - 1) / kOutPxPerWarp;
+  constexpr int NW = M3Cfg<FMT>::NW;
+  const int R = m3_height<FMT>(ri);
+  const int tiles = (m->W + M3Cfg<FMT>::OUT - 1) / M3Cfg<FMT>::OUT;
   M3Plan p{};
   p.ri = ri;
   p.bands = (m->H + R - 1) / R;
@@ -1355,12 +1454,12 @@ M3Plan m3_plan(const df_motion* m, int frames, int ri) {
   const int per_slice = tiles * p.bands;  // warp tasks per temporal chunk
   // Temporal chunks (one warp task per (tile, band, chunk)): as many as fit
   // ONE wave of warps (a partial second wave would double the step time).
-  p.slices = std::max(1, slots * kM3Warps / per_slice);
+  p.slices = std::max(1, slots * NW / per_slice);
   p.chunks = std::min(p.slices, frames);
-  if (kM3Warps == 4 && p.chunks > 4) p.chunks &= ~3;  // whole CTAs of one (tile, band)
+  if (NW == 4 && p.chunks > 4) p.chunks &= ~3;  // whole CTAs of one (tile, band)
   p.chunk = (frames + p.chunks - 1) / p.chunks;
   p.chunks = (frames + p.chunk - 1) / p.chunk;
-  const int ctas = (per_slice * p.chunks + kM3Warps - 1) / kM3Warps;
+  const int ctas = (per_slice * p.chunks + NW - 1) / NW;
   const int waves = (ctas + slots - 1) / slots;
   p.cost = (double)waves * (p.chunk + (p.chunks > 1 ? 1 : 0)) * (R + 6);
   return p;
@@ -1369,14 +1468,15 @@ M3Plan m3_plan(const df_motion* m, int frames, int ri) {
 template <int FMT>
 int launch_m3(df_motion* m, const MotionIO& io, int frames, cudaStream_t s) {
   MotionGeom g = make_geom(m, frames);
-  M3Plan best = m3_plan(m, frames, 0);
+  constexpr int NW = M3Cfg<FMT>::NW;
+  M3Plan best = m3_plan<FMT>(m, frames, 0);
   for (int ri = 1; ri < 3; ++ri) {
-    const M3Plan p = m3_plan(m, frames, ri);
+    const M3Plan p = m3_plan<FMT>(m, frames, ri);
     if (p.cost < best.cost) best = p;
   }
   if (const char* force = getenv("DF_MOTION_M3_R")) {  // tests: pin the band height
     const int ri = atoi(force);
-    if (ri >= 0 && ri < 3) best = m3_plan(m, frames, ri);
+    if (ri >= 0 && ri < 3) best = m3_plan<FMT>(m, frames, ri);
   }
   g.chunk = best.chunk;
   g.m3_chunks = best.chunks;
@@ -1411,15 +1511,16 @@ int launch_m3(df_motion* m, const MotionIO& io, int frames, cudaStream_t s) {
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     DF_REQUIRE(cr == CUDA_SUCCESS, DF_ECUDA, "motion: cuTensorMapEncodeTiled (halo) failed (%d)", (int)cr);
   }
-  const int tiles = (m->W + kOutPxPerWarp - 1) / kOutPxPerWarp;
-  dim3 grid((tiles * best.bands * best.chunks + kM3Warps - 1) / kM3Warps);
+  const int tiles = (m->W + M3Cfg<FMT>::OUT - 1) / M3Cfg<FMT>::OUT;
+  dim3 grid((tiles * best.bands * best.chunks + NW - 1) / NW);
   if (getenv("DF_DEBUG"))
-    fprintf(stderr, "motion_m3: R %d, resident %d/SM, grid %ux%ux%u, chunk %d frames, smem %zu\n",
-            kM3Heights[best.ri], m->m3_resident[best.ri], grid.x, grid.y, grid.z, g.chunk, m3_smem_bytes<FMT>());
+    fprintf(stderr, "motion_m3: %d px/lane, %d warps, R %d, resident %d/SM, grid %ux%ux%u, chunk %d frames, smem %zu\n",
+            M3Cfg<FMT>::PX, NW, m3_height<FMT>(best.ri), m->m3_resident[best.ri], grid.x, grid.y, grid.z, g.chunk,
+            m3_smem_bytes<FMT>());
   const size_t smem = m3_smem_bytes<FMT>();
   cudaLaunchConfig_t lc{};
   lc.gridDim = grid;
-  lc.blockDim = dim3(32 * kM3Warps);
+  lc.blockDim = dim3(32 * NW);
   lc.dynamicSmemBytes = smem;
   lc.stream = s;
   cudaLaunchAttribute attr[1];
@@ -1429,11 +1530,11 @@ int launch_m3(df_motion* m, const MotionIO& io, int frames, cudaStream_t s) {
   lc.numAttrs = DF_M3_PDL ? 1 : 0;
   cudaError_t le;
   if (best.ri == 0)
-    le = cudaLaunchKernelEx(&lc, motion_m3_kernel<FMT, kM3Heights[0]>, map, hmap, io, g, m->scratch);
+    le = cudaLaunchKernelEx(&lc, motion_m3_kernel<FMT, m3_height<FMT>(0)>, map, hmap, io, g, m->scratch);
   else if (best.ri == 1)
-    le = cudaLaunchKernelEx(&lc, motion_m3_kernel<FMT, kM3Heights[1]>, map, hmap, io, g, m->scratch);
+    le = cudaLaunchKernelEx(&lc, motion_m3_kernel<FMT, m3_height<FMT>(1)>, map, hmap, io, g, m->scratch);
   else
-    le = cudaLaunchKernelEx(&lc, motion_m3_kernel<FMT, kM3Heights[2]>, map, hmap, io, g, m->scratch);
+    le = cudaLaunchKernelEx(&lc, motion_m3_kernel<FMT, m3_height<FMT>(2)>, map, hmap, io, g, m->scratch);
   DF_CHECK_CUDA(le);
   return after_launch("motion_m3_kernel");
 }
@@ -1501,7 +1602,8 @@ int df_motion_create(int device, unsigned width, unsigned height, int fmt, uint8
         cudaFuncAttributes fa{};
         if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, f3);
         if (e == cudaSuccess) {
-          const int by_regs = 65536 / std::max(1, fa.numRegs * 32 * kM3Warps);
+          const int nw = fmt == DF_MOTION_RGB ? M3Cfg<DF_MOTION_RGB>::NW : M3Cfg<DF_MOTION_GRAY>::NW;
+          const int by_regs = 65536 / std::max(1, fa.numRegs * 32 * nw);
           const int by_smem = smem_sm / (sm3 + (int)fa.sharedSizeBytes + 1024);
           m->m3_resident[ri] = std::max(0, std::min({512 / kTmemCols, by_regs, by_smem}));
         }
