@@ -659,12 +659,15 @@ constexpr int kM3Warps = DF_M3_WARPS;
 #ifndef DF_M3_GRAY_PX
 #define DF_M3_GRAY_PX 16
 #endif
+#ifndef DF_M3_RGB_PX
+#define DF_M3_RGB_PX 8
+#endif
 #ifndef DF_M3_WIDE_WARPS
 #define DF_M3_WIDE_WARPS 12
 #endif
 template <int FMT>
 struct M3Cfg {
-  static constexpr int PX = FMT == DF_MOTION_GRAY ? DF_M3_GRAY_PX : kPxPerLane;  // px per lane
+  static constexpr int PX = FMT == DF_MOTION_GRAY ? DF_M3_GRAY_PX : DF_M3_RGB_PX;  // px per lane
   static constexpr int WPL = PX / 4;                                            // gray words per lane
   static constexpr int NW = PX == 16 ? DF_M3_WIDE_WARPS : kM3Warps;             // warps per CTA
   static constexpr int OUT = 30 * PX;                                           // output px per warp tile
@@ -674,8 +677,12 @@ struct M3Cfg {
   // the tile row plus 8 bytes on both sides; aligned for gray PX = 16.
   static constexpr int LEAD = (PX * FMT) % 16 == 0 ? 0 : 8;
   static constexpr int BPL = PX * FMT;  // input bytes per lane per row
+  // TMA element size: a box dimension holds at most 256 elements, so rows
+  // wider than 1 KB (RGB at 16 px per lane: 1536 B) use 8-byte elements.
+  static constexpr int ESZ = (32 * BPL + 2 * LEAD) / 4 > 256 ? 8 : 4;
 };
 static_assert(DF_M3_GRAY_PX == 8 || DF_M3_GRAY_PX == 16, "gray px per lane");
+static_assert(DF_M3_RGB_PX == 8 || DF_M3_RGB_PX == 16, "RGB px per lane");
 // Band heights R (template parameter): a frame pass fetches rows y0-3 ..
 // y0+R+2 (R + 6 rows, whole 5-row boxes), gauss(prev) holds R + 2 rows in
 // WPL(R + 2) TMEM columns per warp.  launch_m3 picks R per frame geometry.
@@ -960,9 +967,12 @@ __device__ __forceinline__ void m3_pass(M3Stream<FMT, R>& st, unsigned char* __r
   auto fetch = [&](int k, unsigned (&w)[NIN]) {
     if (k == 0) st.acquire();
     const unsigned a = st.row(k);
-    if constexpr (NIN == 4) {
-      const uint4 v = lds128(a);
-      w[0] = v.x, w[1] = v.y, w[2] = v.z, w[3] = v.w;
+    if constexpr (NIN % 4 == 0) {
+#pragma unroll
+      for (int i = 0; i < NIN / 4; ++i) {
+        const uint4 v = lds128(a + 16 * i);
+        w[4 * i] = v.x, w[4 * i + 1] = v.y, w[4 * i + 2] = v.z, w[4 * i + 3] = v.w;
+      }
     } else {
 #pragma unroll
       for (int i = 0; i < NIN / 2; ++i) {
@@ -974,8 +984,8 @@ __device__ __forceinline__ void m3_pass(M3Stream<FMT, R>& st, unsigned char* __r
   auto finish = [&](M3Row<WPL>& r, int k, const unsigned (&w)[NIN]) {
     unsigned gw[WPL];
     if constexpr (FMT == DF_MOTION_RGB) {
-      gw[0] = rgb4_to_gray(w[0], w[1], w[2], g.wg);
-      gw[1] = rgb4_to_gray(w[3], w[4], w[5], g.wg);
+#pragma unroll
+      for (int i = 0; i < WPL; ++i) gw[i] = rgb4_to_gray(w[3 * i], w[3 * i + 1], w[3 * i + 2], g.wg);
     } else {
 #pragma unroll
       for (int i = 0; i < WPL; ++i) gw[i] = w[i];
@@ -1182,7 +1192,7 @@ __global__ void __launch_bounds__(32 * M3Cfg<FMT>::NW, DF_M3_MINB) motion_m3_ker
   st.stage = 0;
   st.phase = 0;
   st.cur = 0;
-  st.c0 = (tx0 * FMT - Cfg::LEAD) / 4;  // 16-byte aligned box start (see M3Cfg::LEAD)
+  st.c0 = (tx0 * FMT - Cfg::LEAD) / Cfg::ESZ;  // 16-byte aligned box start (see M3Cfg::LEAD)
   st.l2hint = g.l2hint;
   st.H = g.H;
   st.y0 = y0;
@@ -1492,21 +1502,22 @@ int launch_m3(df_motion* m, const MotionIO& io, int frames, cudaStream_t s) {
       io.channel_mode ? chan_capacity_tokens(io.in_ch.rate, io.in_ch.has_delay) : (unsigned long long)frames;
   CUtensorMap map;
 #if DF_M3_TMA3D
-  const cuuint64_t dims[3] = {(cuuint64_t)m->W * FMT / 4, (cuuint64_t)m->H, (cuuint64_t)map_frames};
+  const cuuint64_t dims[3] = {(cuuint64_t)m->W * FMT / M3Cfg<FMT>::ESZ, (cuuint64_t)m->H, (cuuint64_t)map_frames};
 #else
-  const cuuint64_t dims[3] = {(cuuint64_t)m->W * FMT / 4, (cuuint64_t)m->H * map_frames, 1};
+  const cuuint64_t dims[3] = {(cuuint64_t)m->W * FMT / M3Cfg<FMT>::ESZ, (cuuint64_t)m->H * map_frames, 1};
 #endif
   const cuuint64_t strides[2] = {(cuuint64_t)m->W * FMT, (cuuint64_t)m->W * FMT * (cuuint64_t)m->H};
-  const cuuint32_t box[3] = {(cuuint32_t)(m3_row_bytes<FMT>() / 4), (cuuint32_t)kM3RPS, 1};
+  const cuuint32_t box[3] = {(cuuint32_t)(m3_row_bytes<FMT>() / M3Cfg<FMT>::ESZ), (cuuint32_t)kM3RPS, 1};
+  const CUtensorMapDataType dtype = M3Cfg<FMT>::ESZ == 8 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_UINT32;
   const cuuint32_t estr[3] = {1, 1, 1};
-  CUresult cr = tensor_map_encoder()(&map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<void*>(base), dims,
+  CUresult cr = tensor_map_encoder()(&map, dtype, 3, const_cast<void*>(base), dims,
                                      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   DF_REQUIRE(cr == CUDA_SUCCESS, DF_ECUDA, "motion: cuTensorMapEncodeTiled failed (%d)", (int)cr);
   CUtensorMap hmap = map;
   if (io.halo) {  // one frame, same box
-    const cuuint64_t hdims[3] = {(cuuint64_t)m->W * FMT / 4, (cuuint64_t)m->H, 1};
-    cr = tensor_map_encoder()(&hmap, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<unsigned char*>(io.halo), hdims,
+    const cuuint64_t hdims[3] = {(cuuint64_t)m->W * FMT / M3Cfg<FMT>::ESZ, (cuuint64_t)m->H, 1};
+    cr = tensor_map_encoder()(&hmap, dtype, 3, const_cast<unsigned char*>(io.halo), hdims,
                               strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     DF_REQUIRE(cr == CUDA_SUCCESS, DF_ECUDA, "motion: cuTensorMapEncodeTiled (halo) failed (%d)", (int)cr);

@@ -125,15 +125,42 @@ def test_kernel_selection(gpu):
     assert motion.MotionActor(33, 29, motion.GRAY).kernel_name == "motion_fused_kernel"
 
 
-@pytest.mark.parametrize("h", [5, 6, 7, 53, 54, 55, 59, 60, 61, 108, 109, 113, 115])
+@pytest.mark.parametrize("h", [5, 6, 7, 28, 29, 30, 34, 35, 39, 40, 41, 44, 49, 50, 53, 54, 55, 59, 60, 61, 78, 79,
+                               108, 109, 113, 115])
 @pytest.mark.parametrize("ri", [0, 1, 2])
 def test_tma_tmem_heights_near_band_edges(gpu, monkeypatch, ri, h):
-    # Frame heights around the band heights (49/54/59): last bands of 1..R
-    # rows, bands entirely in the border, interior/general band mixes.
+    # Frame heights around the band heights (gray, 16 px per lane: 29/34/39;
+    # RGB: 39/44/49): last bands of 1..R rows, bands entirely in the border,
+    # interior/general band mixes.
     monkeypatch.setenv("DF_MOTION_M3_R", str(ri))
     w, n = 256, 3
     f = O.synth_bytes(n * w * h, 1000 * ri + h)
     assert_frames_equal(run_gpu(f, w, h, chunk=2), O.motion_gray(f, w, h), w, h)
+
+
+@pytest.mark.parametrize("w", [16, 32, 464, 480, 496, 960, 976, 1296])
+@pytest.mark.parametrize("h", [5, 40, 79])
+def test_gray_wide_lane_tiles(gpu, w, h):
+    # Gray runs the TMA/TMEM kernel at 16 px per lane (480-px tiles, 12-warp
+    # CTAs): frames narrower than a tile, exactly one or two tiles, a last
+    # tile holding a single 16-px lane, and the frame edge inside a lane word.
+    from paper_1611_03226_b200 import motion
+    assert motion.MotionActor(w, h, motion.GRAY).kernel_name == "motion_m3_kernel"
+    n = 4
+    f = O.synth_bytes(n * w * h, 7 * w + h)
+    assert_frames_equal(run_gpu(f, w, h, chunk=3), O.motion_gray(f, w, h), w, h)
+
+
+@pytest.mark.parametrize("thr", [0, 1, 127, 128, 254, 255])
+def test_tma_tmem_gray_thresholds_structured(gpu, thr):
+    w, h, n = 512, 140, 7
+    yy, xx = np.mgrid[0:h, 0:w]
+    frames = np.stack([((xx * 3 + yy + 13 * t) % 256) for t in range(n)]).astype(np.uint8)
+    frames[3, 20:90, 100:400] = 255
+    frames[5, :, 0:2] = 0
+    frames[5, :, w - 2:] = 255
+    f = frames.reshape(-1)
+    assert_frames_equal(run_gpu(f, w, h, thr), O.motion_gray(f, w, h, thr), w, h)
 
 
 @pytest.mark.parametrize("thr", [0, 1, 127, 128, 254, 255])
