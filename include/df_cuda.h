@@ -174,6 +174,10 @@ int df_dpd_create(int device, uint32_t period, uint32_t taps_per_branch,
 int df_dpd_destroy(df_dpd* dpd);
 int df_dpd_set_taps(df_dpd* dpd, const float* taps_host, void* stream);
 int df_dpd_reset(df_dpd* dpd, void* stream); /* zero FIR history */
+/* Name of the main kernel the actor's last firing launched ("dpd_wave_kernel"
+ * for grids that fit one wave, else "dpd_main_kernel" / "dpd_main_generic_kernel";
+ * "" before the first firing).  Static storage. */
+const char* df_dpd_kernel_name(const df_dpd* dpd);
 /* Reads the FIR history (10 branches x (T-1) complex) to host; synchronizes. */
 int df_dpd_get_state(df_dpd* dpd, float* state_host);
 int df_dpd_error(df_dpd* dpd); /* sticky device error word; synchronizes */

@@ -120,6 +120,7 @@ _SIGS = {
     "df_dpd_destroy": (_i, [_vp]),
     "df_dpd_set_taps": (_i, [_vp, _vp, _vp]),
     "df_dpd_reset": (_i, [_vp, _vp]),
+    "df_dpd_kernel_name": (C.c_char_p, [_vp]),
     "df_dpd_get_state": (_i, [_vp, _vp]),
     "df_dpd_error": (_i, [_vp]),
     "df_dpd_set_history": (_i, [_vp, _vp, _u32, _u32, _vp]),

@@ -926,6 +926,7 @@ struct df_dpd {
   float2* state = nullptr;     // device, 10*(kMaxTaps-1): FirState per branch
   unsigned resident_ctas = 0;  // main-kernel CTAs resident on the device (prefetch distance)
   unsigned resident_wave_ctas = 0;  // dpd_wave_kernel CTAs resident on the device (one wave)
+  const char* last_kernel = "";     // main kernel of the last firing (df_dpd_kernel_name)
   unsigned* scratch = nullptr; // [0] error word, [1] done counter, [4..13] fast-path last1
   float2* hist = nullptr;      // device history table, capacity hist_blocks
   int* act = nullptr;          // device active lists, 10*hist_blocks
@@ -1008,6 +1009,7 @@ int launch_dpd(df_dpd* d, const DpdIO& io, unsigned long long K, cudaStream_t s,
                                              err, done, fs)
                         : cudaLaunchKernelEx(&lc, dpd_wave_kernel<10, kV, kThreads, false>, io, d->taps, d->period,
                                              err, done, fs));
+    d->last_kernel = "dpd_wave_kernel";
     DF_TRY(after_launch("dpd_wave_kernel"));
   } else if (d->T == 10 || d->T == 32) {
     constexpr int S = kThreads * kV;
@@ -1057,6 +1059,7 @@ int launch_dpd(df_dpd* d, const DpdIO& io, unsigned long long K, cudaStream_t s,
              : halo ? cudaLaunchKernelEx(&lc, dpd_main_kernel<32, kV, kThreads, true, true>, sub, tp, hist, d->period, bm, ahead, err, done, fs)
                     : cudaLaunchKernelEx(&lc, dpd_main_kernel<32, kV, kThreads, true, false>, sub, tp, hist, d->period, bm, ahead, err, done, fs);
       DF_CHECK_CUDA(le);
+      d->last_kernel = "dpd_main_kernel";
       DF_TRY(after_launch("dpd_main_kernel"));
       // Later sub-launches continue from the state this one advanced (which
       // already holds the halo of branches it never saw active).
@@ -1074,6 +1077,7 @@ int launch_dpd(df_dpd* d, const DpdIO& io, unsigned long long K, cudaStream_t s,
       const float2* hist = d->hist + base * kBranches * std::max<uint32_t>(d->T - 1, 1);
       dim3 grid(std::min<unsigned>((d->period + 255) / 256, 64), (unsigned)k);
       dpd_main_generic_kernel<<<grid, 256, 0, s>>>(sub, d->taps, hist, d->period, (int)d->T, err, done);
+      d->last_kernel = "dpd_main_generic_kernel";
       DF_TRY(after_launch("dpd_main_generic_kernel"));
     }
   }
@@ -1150,6 +1154,8 @@ int df_dpd_set_taps(df_dpd* d, const float* taps_host, void* stream) {
   DF_CHECK_CUDA(cudaStreamSynchronize(as_stream(stream)));
   return DF_OK;
 }
+
+const char* df_dpd_kernel_name(const df_dpd* d) { return d ? d->last_kernel : ""; }
 
 int df_dpd_reset(df_dpd* d, void* stream) {
   DF_REQUIRE(d, DF_EINVAL, "df_dpd_reset: null actor");

@@ -57,6 +57,11 @@ class DpdActor:
         assert t.shape[1] == self.T
         call("df_dpd_set_taps", self.handle, t.ctypes.data_as(C.c_void_p), stream.handle if stream else None)
 
+    @property
+    def kernel_name(self) -> str:
+        """Main kernel of the last firing (df_dpd_kernel_name)."""
+        return lib().df_dpd_kernel_name(self.handle).decode()
+
     def reset(self, stream: Stream | None = None):
         call("df_dpd_reset", self.handle, stream.handle if stream else None)
 

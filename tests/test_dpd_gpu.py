@@ -382,3 +382,29 @@ def test_grid_orders_agree(gpu, T):
     assert np.array_equal(bits(whole), bits(chunked))
     n = 96 * period
     assert_parity(whole[:2 * n], O.dpd(x[:2 * n], taps, sched, period))
+
+
+def test_kernel_name_follows_grid(gpu):
+    """df_dpd_kernel_name names the main kernel of the last firing: the
+    one-wave kernel for a DPD-1-sized batch (2^20 samples, period 4096),
+    the tiled main kernel for a batch over one wave, the generic kernel
+    for tap counts other than 10/32 -- and each output stays bit-exact."""
+    from paper_1611_03226_b200 import dpd
+    taps = O.random_taps(2300, 10)
+    sched = np.array([3], np.uint16)
+    a = dpd.DpdActor(4096, taps)
+    assert a.kernel_name == ""
+    for blocks, want in ((256, "dpd_wave_kernel"), (4096, "dpd_main_kernel")):
+        x = O.synth_samples(4096 * blocks, 2400 + blocks)
+        out = np.empty_like(x)
+        a.reset()
+        a.run_host(np.ascontiguousarray(x, np.float32), out, sched, chunk_blocks=blocks)
+        a.check()
+        assert a.kernel_name == want
+        n = 8 * 4096
+        assert_parity(out[:2 * n], O.dpd(x[:2 * n], taps, sched, 4096))
+    g = dpd.DpdActor(64, O.random_taps(2301, 7))
+    x = O.synth_samples(64 * 16, 2500)
+    out = np.empty_like(x)
+    g.run_host(np.ascontiguousarray(x, np.float32), out, sched)
+    assert g.kernel_name == "dpd_main_generic_kernel"

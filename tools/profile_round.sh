@@ -10,7 +10,7 @@ done
 bash tools/ncu_full.sh motion720 motion_m3_kernel
 bash tools/ncu_full.sh motion720gray motion_m3_kernel
 bash tools/ncu_full.sh motion4k motion_m3_kernel
-bash tools/ncu_full.sh dpd1 dpd_main_kernel
+bash tools/ncu_full.sh dpd1 dpd_wave_kernel
 bash tools/ncu_full.sh dpd3 dpd_main_kernel
 bash tools/ncu_full.sh dpd5 dpd_main_kernel
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:net_kernel -c 1 -o gpurun_out/prof_resident -f \
