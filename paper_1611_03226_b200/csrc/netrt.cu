@@ -386,6 +386,10 @@ __device__ __forceinline__ void batched(const Group& G, unsigned long long n, L 
   }
 }
 
+struct U4x2 {
+  uint4 re, im;
+};
+
 __device__ __noinline__ void copy_bytes(unsigned char* dst, const unsigned char* src, unsigned long long n, const Group& G) {
   if (((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src) | n) & 15) == 0) {
     const uint4* s = reinterpret_cast<const uint4*>(src);
@@ -397,6 +401,19 @@ __device__ __noinline__ void copy_bytes(unsigned char* dst, const unsigned char*
                               [&](unsigned long long k, unsigned char v) { dst[k] = v; });
   }
 }
+
+// DPD split fire on 16-byte words: each word of re and im is loaded once
+// and stored to every active output of its plane.
+__device__ __noinline__ void split_planes(const ActorDesc& A, const Frame& F, const Group& G, unsigned long long n16) {
+  const uint4* re = reinterpret_cast<const uint4*>(F.in_ptr[0]);
+  const uint4* im = reinterpret_cast<const uint4*>(F.in_ptr[1]);
+  batched<2, U4x2>(G, n16, [&](unsigned long long k) { return U4x2{__ldcg(re + k), __ldcg(im + k)}; },
+                   [&](unsigned long long k, const U4x2& v) {
+                     for (unsigned o = 0; o < A.n_out; ++o)
+                       if ((F.out_on >> o) & 1u) reinterpret_cast<uint4*>(F.out_ptr[o])[k] = o & 1u ? v.im : v.re;
+                   });
+}
+
 
 // The branch actor's window: kBranchV consecutive outputs per thread.
 constexpr int kBranchV = 4;
@@ -647,6 +664,17 @@ __device__ void fire_kind(const ActorDesc& A, const Frame& F, const Group& G, Ac
       break;
     }
     case DF_ACT_DPD_SPLIT: {  // dpd.cpp:246-256: inputs 0,1 (re, im) -> active pairs
+      // Every output of a pair carries the same plane: load each 16-byte
+      // word of re and im once and store it to every active output, so a
+      // firing costs one load latency instead of one per active output.
+      const unsigned long long bytes = (unsigned long long)A.in[0].rate * A.in[0].token_size;
+      uintptr_t al = reinterpret_cast<uintptr_t>(F.in_ptr[0]) | reinterpret_cast<uintptr_t>(F.in_ptr[1]) | bytes;
+      for (unsigned o = 0; o < A.n_out; ++o)
+        if ((F.out_on >> o) & 1u) al |= reinterpret_cast<uintptr_t>(F.out_ptr[o]);
+      if ((al & 15) == 0 && A.in[1].rate * A.in[1].token_size == bytes) {
+        split_planes(A, F, G, bytes / 16);
+        break;
+      }
       for (unsigned o = 0; o < A.n_out; ++o)
         if ((F.out_on >> o) & 1u)
           copy_bytes(F.out_ptr[o], F.in_ptr[o & 1], (unsigned long long)A.out[o].rate * A.out[o].token_size, G);
