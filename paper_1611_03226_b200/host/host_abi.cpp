@@ -636,6 +636,30 @@ int dfh_validate_demo(int which) {
       n = (int)validate(build_network(actors, chans)).size();
       return;
     }
+    if (which == 7 || which == 8) {  // batched device_control actor: control rate 4
+      // 7: its regular channels carry 4 tokens per firing too (one control
+      // token per port token): valid.  8: its input carries 1: "control
+      // rate must be 1" (model.cpp:133-134).
+      const std::uint32_t in_rate = which == 7 ? 4 : 1;
+      chans = {{"c", 4, 4, false, {}}, {"x", 16, in_rate, false, {}}, {"y", 16, 4, false, {}}};
+      ActorBehavior src, dyn, snk;
+      src.fire = noop;
+      snk.fire = noop;
+      dyn.fire = noop;
+      dyn.device_control = true;
+      actors.push_back({"src", ActorKind::static_rate,
+                        {{PortDirection::output, PortKind::regular, "c"},
+                         {PortDirection::output, PortKind::regular, "x"}},
+                        src});
+      actors.push_back({"dyn", ActorKind::dynamic_rate,
+                        {{PortDirection::input, PortKind::control, "c"},
+                         {PortDirection::input, PortKind::regular, "x"},
+                         {PortDirection::output, PortKind::regular, "y"}},
+                        dyn});
+      actors.push_back({"snk", ActorKind::static_rate, {{PortDirection::input, PortKind::regular, "y"}}, snk});
+      n = (int)validate(build_network(actors, chans)).size();
+      return;
+    }
     // which == 3: BuildError (unknown channel)
     ActorBehavior b;
     b.fire = noop;

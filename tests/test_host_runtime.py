@@ -24,6 +24,14 @@ def test_cycles_through_rate2_delay_channels_are_violations():
     assert H.validate_demo(6) == 1
 
 
+def test_batched_control_rate_needs_matching_port_rates():
+    # The reference requires control rate 1 (model.cpp:133-134).  A device-
+    # controlled GPU actor may batch r reference firings (r control tokens,
+    # r tokens on every regular port); any other control rate is rejected.
+    assert H.validate_demo(7) == 0
+    assert H.validate_demo(8) == 1
+
+
 def test_unknown_channel_is_build_error():
     assert H.validate_demo(3) == -1
     assert b"BuildError" in H.lib().dfh_last_error()
