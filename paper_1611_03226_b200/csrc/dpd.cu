@@ -1301,7 +1301,7 @@ int df_dpd_run_host(df_dpd* d, const float* in_host, float* out_host, uint64_t s
   DF_REQUIRE(d && in_host && out_host, DF_EINVAL, "df_dpd_run_host: null argument");
   DF_REQUIRE(schedule_host && schedule_len > 0, DF_EINVAL, "dpd: schedule must not be empty");
   DF_REQUIRE(samples % d->period == 0, DF_EINVAL,
-             "dpd: sample count must be a nonzero multiple of the period");
+             "dpd: sample count must be a multiple of the period");
   if (samples == 0) return DF_OK;
   DF_CHECK_CUDA(cudaSetDevice(d->device));
   const uint64_t blocks = samples / d->period;

@@ -408,3 +408,26 @@ def test_kernel_name_follows_grid(gpu):
     out = np.empty_like(x)
     g.run_host(np.ascontiguousarray(x, np.float32), out, sched)
     assert g.kernel_name == "dpd_main_generic_kernel"
+
+
+def test_empty_firings_keep_the_fir_state(gpu):
+    """Zero samples / zero blocks fire nothing: the FIR history, the
+    run_host schedule position and the output of the next firing are
+    unchanged (oracle over the whole stream)."""
+    from paper_1611_03226_b200 import dpd
+    from paper_1611_03226_b200.device import Buffer
+    period, blocks = 64, 12
+    x = O.synth_samples(period * blocks, 2600)
+    taps = O.random_taps(2601)
+    sched = np.array([3, 0x3FF, 0x101, 6, 0x200], np.uint16)
+    want = O.dpd(x, taps, sched, period)
+    a = dpd.DpdActor(period, taps)
+    got = np.empty_like(x)
+    h = 2 * period * 5
+    a.run_host(np.ascontiguousarray(x[:h]), got[:h], sched)
+    a.run_host(np.empty(0, np.float32), np.empty(0, np.float32), sched)
+    scratch = Buffer(64)
+    a.fire(scratch, scratch, scratch, 0)
+    a.run_host(np.ascontiguousarray(x[h:]), got[h:], sched)
+    a.check()
+    assert_parity(got, want)

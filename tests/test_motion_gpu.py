@@ -296,3 +296,23 @@ def test_channel_bound_firing_with_delay_channel(gpu):
     assert st.tokens_written == rounds and st.tokens_read == rounds and st.tokens_available == 1
     assert st.write_phase == rounds % 3 and st.read_phase == rounds % 3
     assert_frames_equal(got, O.motion_rgb(f, w, h), w, h)
+
+
+def test_empty_firings_keep_the_delay_token(gpu):
+    """Zero frames (the reference's network with frames = 0 fires nothing,
+    motion.cpp:104) is a no-op at every entry point: a zero-frame fire or
+    run_host between two runs changes neither the output nor the delay
+    token the next firing diffs against."""
+    from paper_1611_03226_b200 import motion
+    from paper_1611_03226_b200.device import Buffer
+    w, h, n = 96, 40, 6
+    f = O.synth_bytes(n * w * h, 77)
+    want = O.motion_gray(f, w, h, 32)
+    a = motion.MotionActor(w, h, motion.GRAY, 32)
+    got = np.empty(n * w * h, np.uint8)
+    a.run_host(f[: 3 * w * h], got[: 3 * w * h])
+    a.run_host(f[:0], got[:0])
+    scratch = Buffer(w * h)
+    a.fire(scratch, scratch, 0)
+    a.run_host(f[3 * w * h:], got[3 * w * h:])
+    assert_frames_equal(got, want, w, h)
