@@ -809,12 +809,16 @@ def resident_networks():
     ms = [H.dpd_run_resident(x, taps, [3], 65536, branch_ctas=32)[1] for _ in range(3)]
     f = O.synth_bytes(300 * 1280 * 720, 5)
     mm = [H.motion_run_resident(f, 1280, 720, 32, ctas=96)[1] for _ in range(2)]
+    mr = [H.motion_run_resident(f, 1280, 720, 32, rate=10, ctas=96)[1] for _ in range(2)]
     return {"dpd1": {"value": round((1 << 20) / (statistics.median(ms) / 1e3) / 1e6, 1), "unit": "Msamples/s",
                      "path": "dfh_dpd_run_resident: source, config, split, 10 branches, adder, sink (56 channels), "
                              "32 CTAs per branch"},
             "motion720gray": {"value": round(300 / (statistics.median(mm) / 1e3), 1), "unit": "frames/s",
                               "path": "dfh_motion_run_resident: source, gauss, thres, med, sink with the "
                                       "gauss_thres_prev delay channel, 480 CTAs shared by work (gauss 160, med 120, thres 80, source / sink 60)"},
+            "motion720gray_rate10": {"value": round(300 / (statistics.median(mr) / 1e3), 1), "unit": "frames/s",
+                                     "path": "the same network at token rate 10 (10 frames per token: the reference's "
+                                             "--rate option, bench.cpp:212)"},
             "metric": "units / sink-active seconds (bench.cpp:341-347, :391-397), device timestamps"}
 
 

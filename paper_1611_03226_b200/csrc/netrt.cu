@@ -624,6 +624,98 @@ __device__ void fire_median4(const ActorDesc& A, const Frame& F, const Group& G,
   }
 }
 
+// 16 px per thread (frames with W % 16 == 0, 16-byte aligned regions): one
+// 16-byte load per row plus the two neighbour words, so a gauss output word
+// costs 15/4 load requests instead of 15, a median word 5/4 instead of 5.
+#ifndef DF_NET_V16
+#define DF_NET_V16 1
+#endif
+__device__ void fire_gauss16(const ActorDesc& A, const Frame& F, const Group& G, unsigned W, unsigned H) {
+  const unsigned Wc = W / 16, Wq = W / 4;
+  const unsigned long long Sc = (unsigned long long)Wc * H, Sq = (unsigned long long)Wq * H, total = Sc * A.in[0].rate;
+  for (unsigned long long k = G.first(); k < total; k += G.step()) {
+    const unsigned long long f = k / Sc, idx = k % Sc;
+    const unsigned y = (unsigned)(idx / Wc), xc = (unsigned)(idx % Wc);
+    const unsigned* fr = reinterpret_cast<const unsigned*>(F.in_ptr[0]) + f * Sq;  // frame f, in words
+    const unsigned long long cw = (unsigned long long)y * Wq + 4ull * xc;          // this chunk's first word
+    const uint4 c = __ldcg(reinterpret_cast<const uint4*>(fr + cw));
+    uint4 v = c;  // rows y < 2 or >= H-2: gray copied (motion.cpp:34-37)
+    if (y >= 2 && y < H - 2) {
+      unsigned a0[4] = {0, 0, 0, 0}, a1[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int dy = -2; dy <= 2; ++dy) {
+        const unsigned* row = fr + cw + (long long)dy * Wq;
+        const uint4 C = dy == 0 ? c : __ldcg(reinterpret_cast<const uint4*>(row));
+        const unsigned L = xc > 0 ? __ldcg(row - 1) : 0u, R = xc + 1 < Wc ? __ldcg(row + 4) : 0u;
+        const unsigned w = dy == 0 ? 6u : (dy == -1 || dy == 1) ? 4u : 1u;
+        unsigned p01, p23;
+        m_hgauss4(L, C.x, C.y, p01, p23);
+        a0[0] += w * p01, a1[0] += w * p23;
+        m_hgauss4(C.x, C.y, C.z, p01, p23);
+        a0[1] += w * p01, a1[1] += w * p23;
+        m_hgauss4(C.y, C.z, C.w, p01, p23);
+        a0[2] += w * p01, a1[2] += w * p23;
+        m_hgauss4(C.z, C.w, R, p01, p23);
+        a0[3] += w * p01, a1[3] += w * p23;
+      }
+      // (sum + 128) >> 8 per px: byte 1 of each 16-bit lane
+      v = make_uint4(m_prmt(a0[0], a1[0], 0x7531), m_prmt(a0[1], a1[1], 0x7531), m_prmt(a0[2], a1[2], 0x7531),
+                     m_prmt(a0[3], a1[3], 0x7531));
+      // Columns x < 2 or x >= W-2: gray copied.
+      if (xc == 0) v.x = (v.x & 0xFFFF0000u) | (c.x & 0x0000FFFFu);
+      if (xc + 1 == Wc) v.w = (v.w & 0x0000FFFFu) | (c.w & 0xFFFF0000u);
+    }
+    for (unsigned o = 0; o < A.n_out; ++o) {
+      reinterpret_cast<uint4*>(F.out_ptr[o])[k] = v;
+      // Fig. 2 phase-2 copy (slot 3r -> slot 0, channel.cpp:97-104) done by
+      // the writer of each chunk instead of the leader CTA afterwards.
+      const unsigned long long last = (unsigned long long)(A.out[o].rate - 1) * Sc;
+      if (((F.out_wrap >> o) & 1u) && k >= last) reinterpret_cast<uint4*>(A.out[o].storage)[k - last] = v;
+    }
+  }
+}
+
+__device__ __forceinline__ unsigned m_med5w(unsigned c, unsigned up, unsigned dn, unsigned lw, unsigned rw) {
+  unsigned a = c, b = up, cc = dn;
+  unsigned d = __funnelshift_l(lw, c, 8), e = __funnelshift_r(c, rw, 8);  // left / right neighbours
+  // median of 5 per byte: the scalar actor's sorting network on 4 lanes
+  m_sort2(a, b); m_sort2(d, e); m_sort2(a, cc); m_sort2(b, cc); m_sort2(a, d);
+  m_sort2(cc, d); m_sort2(b, e); m_sort2(b, cc); m_sort2(d, e);
+  return cc;
+}
+
+__device__ void fire_median16(const ActorDesc& A, const Frame& F, const Group& G, unsigned W, unsigned H) {
+  const unsigned Wc = W / 16, Wq = W / 4;
+  const unsigned long long Sc = (unsigned long long)Wc * H, Sq = (unsigned long long)Wq * H, total = Sc * A.in[0].rate;
+  for (unsigned long long k = G.first(); k < total; k += G.step()) {
+    const unsigned long long f = k / Sc, idx = k % Sc;
+    const unsigned y = (unsigned)(idx / Wc), xc = (unsigned)(idx % Wc);
+    const unsigned* fr = reinterpret_cast<const unsigned*>(F.in_ptr[0]) + f * Sq;
+    const unsigned long long cw = (unsigned long long)y * Wq + 4ull * xc;
+    const uint4 c = __ldcg(reinterpret_cast<const uint4*>(fr + cw));
+    uint4 v = c;  // rows 0 and H-1: copied (motion.cpp:64-67)
+    if (y >= 1 && y < H - 1) {
+      const uint4 u = __ldcg(reinterpret_cast<const uint4*>(fr + cw - Wq));
+      const uint4 dn = __ldcg(reinterpret_cast<const uint4*>(fr + cw + Wq));
+      const unsigned lw = xc > 0 ? __ldcg(fr + cw - 1) : 0u, rw = xc + 1 < Wc ? __ldcg(fr + cw + 4) : 0u;
+      v.x = m_med5w(c.x, u.x, dn.x, lw, c.y);
+      v.y = m_med5w(c.y, u.y, dn.y, c.x, c.z);
+      v.z = m_med5w(c.z, u.z, dn.z, c.y, c.w);
+      v.w = m_med5w(c.w, u.w, dn.w, c.z, rw);
+      if (xc == 0) v.x = (v.x & 0xFFFFFF00u) | (c.x & 0xFFu);              // column 0 copied
+      if (xc + 1 == Wc) v.w = (v.w & 0x00FFFFFFu) | (c.w & 0xFF000000u);   // column W-1 copied
+    }
+    reinterpret_cast<uint4*>(F.out_ptr[0])[k] = v;
+  }
+}
+
+__device__ __forceinline__ bool chunks16_ok(const Frame& F, const ActorDesc& A, unsigned W) {
+  uintptr_t m = W & 15u;
+  for (unsigned p = 0; p < A.n_in; ++p) m |= reinterpret_cast<uintptr_t>(F.in_ptr[p]);
+  for (unsigned p = 0; p < A.n_out; ++p) m |= reinterpret_cast<uintptr_t>(F.out_ptr[p]) | reinterpret_cast<uintptr_t>(A.out[p].storage);
+  return DF_NET_V16 && (m & 15u) == 0;
+}
+
 __device__ __forceinline__ bool words_ok(const Frame& F, const ActorDesc& A, unsigned W) {
   uintptr_t m = W & 3u;
   for (unsigned p = 0; p < A.n_in; ++p) m |= reinterpret_cast<uintptr_t>(F.in_ptr[p]);
@@ -754,6 +846,10 @@ __device__ void fire_kind(const ActorDesc& A, const Frame& F, const Group& G, Ac
     case DF_ACT_GAUSS: {  // gauss5x5 (motion.cpp:27-48) of every frame, to every output
       const df_act_frames& P = params<df_act_frames>(A);
       const unsigned W = P.width, H = P.height;
+      if (W >= 32 && H >= 5 && chunks16_ok(F, A, W)) {
+        fire_gauss16(A, F, G, W, H);
+        break;
+      }
       if (W >= 8 && H >= 5 && words_ok(F, A, W)) {
         fire_gauss4(A, F, G, W, H);
         break;
@@ -806,6 +902,10 @@ __device__ void fire_kind(const ActorDesc& A, const Frame& F, const Group& G, Ac
     case DF_ACT_MEDIAN: {  // median5 (motion.cpp:59-74): plus-shaped median, 1-px border copy
       const df_act_frames& P = params<df_act_frames>(A);
       const unsigned W = P.width, H = P.height;
+      if (W >= 32 && H >= 3 && chunks16_ok(F, A, W)) {
+        fire_median16(A, F, G, W, H);
+        break;
+      }
       if (W >= 8 && H >= 3 && words_ok(F, A, W)) {
         fire_median4(A, F, G, W, H);
         break;

@@ -116,10 +116,11 @@ def test_resident_motion_fixture_64x48(gpu, small):
     assert fir == {"source": 16, "gauss": 16, "thres": 16, "med": 16, "sink": 16}
 
 
-@pytest.mark.parametrize("w,h", [(40, 9), (8, 5), (37, 23), (1280, 72)])
+@pytest.mark.parametrize("w,h", [(40, 9), (8, 5), (37, 23), (1280, 72), (32, 5), (48, 5), (64, 7), (336, 41)])
 def test_resident_motion_sizes_vs_oracle(gpu, w, h):
-    # Word-wise gauss/median actors (W % 4 == 0: 40x9, 8x5 at the 5-row /
-    # 8-column minimum, 1280x72) and the byte-wise fallback (37x23).
+    # 16-px gauss/median actors (W % 16 == 0: 1280x72, 32x5 and 48x5 at the
+    # row / column minimum, 64x7 with two chunks per row, 336x41), word-wise
+    # (W % 4 == 0: 40x9, 8x5) and the byte-wise fallback (37x23).
     from paper_1611_03226_b200 import host_api as H
     f = O.synth_bytes(6 * w * h, 7000 + w)
     out, _, _ = H.motion_run_resident(f, w, h, 32, ctas=4)
