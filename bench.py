@@ -801,13 +801,15 @@ def resident_networks():
     -- measured by the reference's metric (units / active_seconds("sink")).
     DPD-1's full configuration; motion 1280x720 x 300 in the reference's
     gray format (that network has no RGB front end)."""
-    from oracle import oracle as O
     from paper_1611_03226_b200 import host_api as H
-    x = O.synth_samples(1 << 20, 810)
-    taps = O.random_taps(808)
+    # Inputs from the library's copies of the reference's generators
+    # (dfh_synth; the same streams as synth_samples / random_taps /
+    # synth_frames, proj/src/dpd.cpp:467-505, motion.cpp:254-260).
+    x = H.synth("samples", 1 << 20, 810)
+    taps = H.synth("taps", 10, 808).reshape(10, 10, 2)
     H.dpd_run_resident(x, taps, [3], 65536, branch_ctas=32)
     ms = [H.dpd_run_resident(x, taps, [3], 65536, branch_ctas=32)[1] for _ in range(3)]
-    f = O.synth_bytes(300 * 1280 * 720, 5)
+    f = H.synth("frames", 300 * 1280 * 720, 5)
     mm = [H.motion_run_resident(f, 1280, 720, 32, ctas=96)[1] for _ in range(2)]
     mr = [H.motion_run_resident(f, 1280, 720, 32, rate=10, ctas=96)[1] for _ in range(2)]
     return {"dpd1": {"value": round((1 << 20) / (statistics.median(ms) / 1e3) / 1e6, 1), "unit": "Msamples/s",

@@ -1,12 +1,13 @@
 """Probe: the reference-shaped networks as device-resident actors (one
 persistent kernel; dfh_*_run_resident) -- sink-active throughput (the
-reference's metric) and wall time, at BASELINE sizes, for a few CTA counts."""
+reference's metric) and wall time, at BASELINE sizes, for a few CTA counts,
+checked against the oracle (so it lives with the tests, not under tools/)."""
 import sys
 import time
 
 import numpy as np
 
-sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))))
+sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__)))))
 from oracle import oracle as O  # noqa: E402
 from paper_1611_03226_b200 import host_api as H  # noqa: E402
 

@@ -1,3 +1,5 @@
+"""Resident DPD-1 at several CTA counts per branch, checked against the
+oracle (run from the repo root)."""
 import sys, os
 sys.path.insert(0, os.getcwd())
 import numpy as np

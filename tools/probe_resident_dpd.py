@@ -8,13 +8,12 @@ import sys
 import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from oracle import oracle as O  # noqa: E402
 from paper_1611_03226_b200 import host_api as H  # noqa: E402
 
-taps = O.random_taps(808)
-x1 = O.synth_samples(1 << 20, 810)
+taps = H.synth("taps", 10, 808).reshape(10, 10, 2)
+x1 = H.synth("samples", 1 << 20, 810)
 ramp = np.array([(1 << (1 + i % 10)) - 1 for i in range(10)], np.uint16)
-x3 = O.synth_samples(1 << int(os.environ.get("LOG2_N3", "22")), 811)
+x3 = H.synth("samples", 1 << int(os.environ.get("LOG2_N3", "22")), 811)
 for bc in [int(c) for c in os.environ.get("BRANCH_CTAS", "8,32").split(",")]:
     for name, x, sched, period in (("dpd1", x1, [3], 65536), ("dpd3", x3, ramp, 4096)):
         best = 0.0

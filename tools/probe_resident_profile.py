@@ -6,15 +6,14 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from oracle import oracle as O  # noqa: E402
 from paper_1611_03226_b200 import host_api as H  # noqa: E402
 
-f = O.synth_bytes(300 * 1280 * 720, 5)
+f = H.synth("frames", 300 * 1280 * 720, 5)
 for ctas in (32, 64, 96):
     out, ms, fir = H.motion_run_resident(f, 1280, 720, 32, rate=1, ctas=ctas)
     print(f"motion ctas={ctas}: {300 / (ms / 1e3):.0f} fps", flush=True)
-x = O.synth_samples(1 << 20, 810)
-taps = O.random_taps(808)
+x = H.synth("samples", 1 << 20, 810)
+taps = H.synth("taps", 10, 808).reshape(10, 10, 2)
 for bc in (16, 32):
     y, ms, fir, _ = H.dpd_run_resident(x, taps, [3], 65536, branch_ctas=bc)
     print(f"dpd1 branch_ctas={bc}: {2**20 / (ms / 1e3) / 1e6:.0f} Msps", flush=True)

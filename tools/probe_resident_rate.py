@@ -7,10 +7,9 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from oracle import oracle as O  # noqa: E402
 from paper_1611_03226_b200 import host_api as H  # noqa: E402
 
-f = O.synth_bytes(300 * 1280 * 720, 5)
+f = H.synth("frames", 300 * 1280 * 720, 5)
 base = None
 for ctas in [int(c) for c in os.environ.get("CTAS", "96").split(",")]:
     for r in [int(c) for c in os.environ.get("RATES", "1,2,5,10,20").split(",")]:
