@@ -59,3 +59,34 @@ def test_l2_rule_every_workload_flushes_or_exceeds_l2():
             assert pooled == (name == "dpd1") == (R > 1), name
         else:
             assert p["w"] * p["h"] * p["fmt"] * p["frames"] > l2, name
+
+
+def test_oracle_only_in_checkers_and_cpu_baseline():
+    """oracle/ is test infrastructure: in bench.py only the CPU-baseline legs
+    (cpu_motion, cpu_dpd) import it, and nothing in the package or tools/
+    does (the product path and the probes never run the checker)."""
+    import ast
+    import pathlib
+    root = pathlib.Path(__file__).resolve().parent.parent
+
+    def importers(path):
+        """Names of the functions (or "<module>") holding an oracle import."""
+        found = []
+
+        def visit(node, owner):
+            for ch in ast.iter_child_nodes(node):
+                if isinstance(ch, (ast.FunctionDef, ast.AsyncFunctionDef)):
+                    visit(ch, ch.name)
+                    continue
+                if isinstance(ch, ast.ImportFrom) and (ch.module or "").split(".")[0] == "oracle":
+                    found.append(owner)
+                elif isinstance(ch, ast.Import) and any(a.name.split(".")[0] == "oracle" for a in ch.names):
+                    found.append(owner)
+                visit(ch, owner)
+
+        visit(ast.parse(path.read_text()), "<module>")
+        return found
+
+    assert set(importers(root / "bench.py")) <= {"cpu_motion", "cpu_dpd"}, importers(root / "bench.py")
+    for path in list((root / "paper_1611_03226_b200").rglob("*.py")) + list((root / "tools").rglob("*.py")):
+        assert not importers(path), path
