@@ -630,6 +630,68 @@ __device__ void fire_median4(const ActorDesc& A, const Frame& F, const Group& G,
 #ifndef DF_NET_V16
 #define DF_NET_V16 1
 #endif
+#ifndef DF_NET_NCH
+#define DF_NET_NCH 2
+#endif
+// NCH adjacent 16-px chunks per thread (the row's chunk count a multiple of
+// NCH): per row NCH 16-byte loads plus the two outer neighbour words.
+template <int NCH>
+__device__ void gauss16_n(const ActorDesc& A, const Frame& F, const Group& G, unsigned W, unsigned H) {
+  const unsigned Wc = W / 16 / NCH, Wq = W / 4;  // Wc: thread items per row
+  const unsigned long long Sc = (unsigned long long)Wc * H, Sq = (unsigned long long)Wq * H, total = Sc * A.in[0].rate;
+  for (unsigned long long k = G.first(); k < total; k += G.step()) {
+    const unsigned long long f = k / Sc, idx = k % Sc;
+    const unsigned y = (unsigned)(idx / Wc), xc = (unsigned)(idx % Wc);
+    const unsigned* fr = reinterpret_cast<const unsigned*>(F.in_ptr[0]) + f * Sq;
+    const unsigned long long cw = (unsigned long long)y * Wq + 4ull * NCH * xc;  // first word of the item
+    uint4 c[NCH];
+#pragma unroll
+    for (int j = 0; j < NCH; ++j) c[j] = __ldcg(reinterpret_cast<const uint4*>(fr + cw) + j);
+    uint4 v[NCH];
+#pragma unroll
+    for (int j = 0; j < NCH; ++j) v[j] = c[j];  // rows y < 2 or >= H-2: gray copied (motion.cpp:34-37)
+    if (y >= 2 && y < H - 2) {
+      unsigned a0[4 * NCH] = {}, a1[4 * NCH] = {};
+#pragma unroll
+      for (int dy = -2; dy <= 2; ++dy) {
+        const unsigned* row = fr + cw + (long long)dy * Wq;
+        unsigned wd[4 * NCH + 2];
+        wd[0] = xc > 0 ? __ldcg(row - 1) : 0u;
+        wd[4 * NCH + 1] = xc + 1 < Wc ? __ldcg(row + 4 * NCH) : 0u;
+#pragma unroll
+        for (int j = 0; j < NCH; ++j) {
+          const uint4 C = dy == 0 ? c[j] : __ldcg(reinterpret_cast<const uint4*>(row) + j);
+          wd[1 + 4 * j] = C.x, wd[2 + 4 * j] = C.y, wd[3 + 4 * j] = C.z, wd[4 + 4 * j] = C.w;
+        }
+        const unsigned w = dy == 0 ? 6u : (dy == -1 || dy == 1) ? 4u : 1u;
+#pragma unroll
+        for (int i = 0; i < 4 * NCH; ++i) {
+          unsigned p01, p23;
+          m_hgauss4(wd[i], wd[i + 1], wd[i + 2], p01, p23);
+          a0[i] += w * p01, a1[i] += w * p23;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < NCH; ++j)
+        v[j] = make_uint4(m_prmt(a0[4 * j], a1[4 * j], 0x7531), m_prmt(a0[4 * j + 1], a1[4 * j + 1], 0x7531),
+                          m_prmt(a0[4 * j + 2], a1[4 * j + 2], 0x7531), m_prmt(a0[4 * j + 3], a1[4 * j + 3], 0x7531));
+      // Columns x < 2 or x >= W-2: gray copied.
+      if (xc == 0) v[0].x = (v[0].x & 0xFFFF0000u) | (c[0].x & 0x0000FFFFu);
+      if (xc + 1 == Wc) v[NCH - 1].w = (v[NCH - 1].w & 0x0000FFFFu) | (c[NCH - 1].w & 0xFFFF0000u);
+    }
+    for (unsigned o = 0; o < A.n_out; ++o) {
+      const unsigned long long last = (unsigned long long)(A.out[o].rate - 1) * Sc;
+      const bool wrap = ((F.out_wrap >> o) & 1u) && k >= last;
+#pragma unroll
+      for (int j = 0; j < NCH; ++j) {
+        reinterpret_cast<uint4*>(F.out_ptr[o])[NCH * k + j] = v[j];
+        // Fig. 2 phase-2 copy (slot 3r -> slot 0, channel.cpp:97-104) by the writer
+        if (wrap) reinterpret_cast<uint4*>(A.out[o].storage)[NCH * (k - last) + j] = v[j];
+      }
+    }
+  }
+}
+
 __device__ void fire_gauss16(const ActorDesc& A, const Frame& F, const Group& G, unsigned W, unsigned H) {
   const unsigned Wc = W / 16, Wq = W / 4;
   const unsigned long long Sc = (unsigned long long)Wc * H, Sq = (unsigned long long)Wq * H, total = Sc * A.in[0].rate;
@@ -846,6 +908,10 @@ __device__ void fire_kind(const ActorDesc& A, const Frame& F, const Group& G, Ac
     case DF_ACT_GAUSS: {  // gauss5x5 (motion.cpp:27-48) of every frame, to every output
       const df_act_frames& P = params<df_act_frames>(A);
       const unsigned W = P.width, H = P.height;
+      if (DF_NET_NCH == 2 && W % 32 == 0 && W >= 64 && H >= 5 && chunks16_ok(F, A, W)) {
+        gauss16_n<2>(A, F, G, W, H);
+        break;
+      }
       if (W >= 32 && H >= 5 && chunks16_ok(F, A, W)) {
         fire_gauss16(A, F, G, W, H);
         break;
